@@ -1,0 +1,130 @@
+/*
+ * wavelcs_capi.h -- C-ABI of the B200-native LCS table-fill library
+ * (libwavelcs_b200.so).  Plain pointers and sizes only; no CUDA, C++ or
+ * torch types cross this boundary.
+ *
+ * Drop-in boundary for the reference "wavelcs" (paths relative to
+ * /root/reference/proj).  Each entry point names the reference interface it
+ * replaces; INTEGRATION.md shows the binding a maintainer adds on the
+ * reference side (a ctypes stub and the C++ facade in include/wavelcs_b200.hpp).
+ *
+ * Conventions
+ *   - x is the "parent" string (DP rows, index i), y the "child" string (DP
+ *     columns, index j), exactly as in lcs_fill_parallel(x, y, cfg)
+ *     (include/wavelcs/parallel.hpp:92-93).  Strings are raw bytes; every
+ *     byte value 0..255 is a symbol (include/wavelcs/sequence.hpp:10-12).
+ *   - Host-pointer entry points are synchronous: results are valid on return.
+ *   - Every call returns a wlcs_status; on failure wlcs_last_error() gives a
+ *     thread-local message.  The C++ facade maps statuses back onto the
+ *     reference's exception types (include/wavelcs/errors.hpp:8-30).
+ *   - The library is re-entrant: each host thread gets its own CUDA stream
+ *     and workspace per device; there is no global mutable state on the fast
+ *     path.  The current CUDA device of the calling thread is used.
+ *   - The CUDA kernels are mandatory: there is no CPU fallback.  Without a
+ *     usable GPU every compute entry point returns WLCS_E_NO_DEVICE.
+ */
+#ifndef WAVELCS_CAPI_H
+#define WAVELCS_CAPI_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define WLCS_ABI_VERSION 1
+
+typedef enum wlcs_status {
+    WLCS_OK = 0,
+    WLCS_E_CAPACITY = 1,         /* wavelcs::CapacityError   (src/tables.cpp:16-23)  */
+    WLCS_E_CONFIG = 2,           /* wavelcs::ConfigError     (src/parallel.cpp:52-54) */
+    WLCS_E_OUT_OF_RANGE = 3,     /* std::out_of_range        (src/serial.cpp:37-41)   */
+    WLCS_E_INVALID_ARGUMENT = 4, /* std::invalid_argument                              */
+    WLCS_E_INPUT = 5,            /* wavelcs::InputError                                */
+    WLCS_E_CUDA = 6,             /* CUDA runtime error                                 */
+    WLCS_E_NO_DEVICE = 7,        /* no usable CUDA device: no CPU fallback exists      */
+    WLCS_E_OUT_OF_MEMORY = 8,    /* device allocation failed                           */
+    WLCS_E_INTERNAL = 9
+} wlcs_status;
+
+/* Budget sentinel: skip the reference's table-capacity check. */
+#define WLCS_NO_BUDGET ((size_t)-1)
+/* kDefaultMemoryBudget (include/wavelcs/tables.hpp:12): 2 GiB. */
+#define WLCS_DEFAULT_BUDGET ((size_t)2 * 1024 * 1024 * 1024)
+
+/* Fill-kernel variants (both give bit-identical lengths). */
+#define WLCS_VARIANT_BITPARALLEL 0 /* Hyyro bit-vector, 32 cells per 3 int ops */
+#define WLCS_VARIANT_WAVEFRONT 1   /* tiled anti-diagonal cell wavefront (DPX) */
+
+int wlcs_abi_version(void);
+const char* wlcs_last_error(void);
+/* Number of visible CUDA devices (0 when none). */
+int wlcs_device_count(void);
+
+/* check_capacity(m, n, budget)  -- include/wavelcs/tables.hpp:16,
+ * src/tables.cpp:9-24: 4(M+1)(N+1) + MN bytes, computed in 128 bits.
+ * Returns WLCS_E_CAPACITY with the reference's message when exceeded. */
+int wlcs_check_capacity(size_t m, size_t n, size_t memory_budget);
+
+/* Length  -- replaces Length lcs_length(const Sequence& x, const Sequence& y,
+ * std::size_t memory_budget)  (include/wavelcs/serial.hpp:24-25,
+ * src/serial.cpp:32-34).  memory_budget keeps the reference's semantics
+ * (CapacityError when the reference's tables would not fit); pass
+ * WLCS_NO_BUDGET to lift it.  The device path itself is O(M + N) memory. */
+int wlcs_length(const uint8_t* x, size_t m, const uint8_t* y, size_t n, size_t memory_budget,
+                uint32_t* out);
+
+/* Same, choosing the fill kernel variant (WLCS_VARIANT_*). */
+int wlcs_length_ex(const uint8_t* x, size_t m, const uint8_t* y, size_t n, size_t memory_budget,
+                   int variant, uint32_t* out);
+
+/* Recovered subsequence  -- replaces the composition the reference's callers
+ * use: lcs_fill_parallel(x, y, cfg) then traceback(fill.back, x, M, N)
+ * (tools/wavelcs_main.cpp:78-86; include/wavelcs/serial.hpp:30,
+ * include/wavelcs/parallel.hpp:92-93).  The result is byte-identical to the
+ * reference's traceback, LEFT tie-break included (include/wavelcs/cell.hpp:27-38).
+ * out must hold at least min(m, n) bytes (cap); *out_len receives the length.
+ * Capacity check as in wlcs_length. */
+int wlcs_subsequence(const uint8_t* x, size_t m, const uint8_t* y, size_t n,
+                     size_t memory_budget, uint8_t* out, size_t cap, size_t* out_len);
+
+/* Batch of independent pairs (new; the reference loops one pair at a time,
+ * src/bench.cpp:77-129).  Pair k is x = xs[x_off[k] .. x_off[k+1]) and
+ * y = ys[y_off[k] .. y_off[k+1]); offsets are absolute, non-decreasing,
+ * pairs + 1 entries each.  out[k] = lcs_length(x_k, y_k).  Host pointers;
+ * page-locked host buffers give full-speed DMA (see wlcs_host_alloc). */
+int wlcs_length_batch(const uint8_t* xs, const uint64_t* x_off, const uint8_t* ys,
+                      const uint64_t* y_off, size_t pairs, uint32_t* out);
+
+/* Same with the kernel variant. */
+int wlcs_length_batch_ex(const uint8_t* xs, const uint64_t* x_off, const uint8_t* ys,
+                         const uint64_t* y_off, size_t pairs, int variant, uint32_t* out);
+
+/* Batch on DEVICE pointers already resident in HBM (current device), enqueued
+ * on `stream` (a cudaStream_t, NULL = the library's per-thread stream).  The
+ * call returns after the results are written to d_out (it synchronises the
+ * stream once to collect pairs that need the single-pair path). */
+int wlcs_length_batch_device(const uint8_t* d_xs, const uint64_t* d_x_off, const uint8_t* d_ys,
+                             const uint64_t* d_y_off, size_t pairs, uint64_t xs_bytes,
+                             uint64_t ys_bytes, int variant, uint32_t* d_out, void* stream);
+
+/* Single pair on DEVICE pointers (length only; budget not applied). */
+int wlcs_length_device(const uint8_t* d_x, size_t m, const uint8_t* d_y, size_t n, int variant,
+                       uint32_t* out, void* stream);
+
+/* Page-locked host memory for zero-copy-speed transfers (cudaHostAlloc). */
+void* wlcs_host_alloc(size_t bytes);
+void wlcs_host_free(void* p);
+
+/* generate_random(length, alphabet, seed)  -- include/wavelcs/io.hpp:34,
+ * src/io.cpp:103-115 (std::mt19937_64, alphabet[rng() % |alphabet|]).
+ * Synthetic-input helper for benchmarks and tests; host-only. */
+int wlcs_generate_random(size_t length, const uint8_t* alphabet, size_t alphabet_len,
+                         uint64_t seed, uint8_t* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* WAVELCS_CAPI_H */

@@ -1,0 +1,76 @@
+// wlcs_common.cuh -- shared device helpers for the B200 LCS kernels.
+//
+// Bit layout used by every bit-parallel kernel (Allison-Dix / Hyyro):
+//   column j (1-based, the "child" / column string) <-> bit (j-1) of V,
+//   word w = (j-1) / 32, bit (j-1) % 32; carries run toward higher columns.
+//   V_0 = all ones; row i: U = V & PM[x_i]; V' = (V + U) | (V & ~PM[x_i]).
+//   DP value c[i][j] = popcount(~V_i & ((1 << j) - 1)),
+//   so LCS = number of zero bits of V_M below column N.
+// This reproduces lcs_cell (proj/include/wavelcs/cell.hpp:30-38) value by
+// value; tests/test_oracle.py checks the identity against the reference.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace wlcs {
+
+constexpr unsigned kFullMask = 0xffffffffu;
+constexpr int kRowsPerStep = 16;  // one 16-byte chunk of the row string per step
+
+// 16 bytes of a string starting at the 16-byte-aligned address `p`.
+// Bytes outside [lo, hi) of the allocation are never touched: when the chunk
+// straddles the allocation end the valid bytes are gathered one by one.
+__device__ __forceinline__ uint4 load_chunk16(const uint8_t* p, const uint8_t* alloc_lo,
+                                              const uint8_t* alloc_hi) {
+    if (p >= alloc_lo && p + 16 <= alloc_hi) {
+        return __ldg(reinterpret_cast<const uint4*>(p));
+    }
+    uint32_t w[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int b = 0; b < 16; ++b) {
+        const uint8_t* q = p + b;
+        if (q >= alloc_lo && q < alloc_hi) w[b >> 2] |= uint32_t(__ldg(q)) << (8 * (b & 3));
+    }
+    return make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+__device__ __forceinline__ uint32_t chunk_byte(const uint4& c, int r) {
+    const uint32_t w = (r < 4) ? c.x : (r < 8) ? c.y : (r < 12) ? c.z : c.w;
+    return (w >> (8 * (r & 3))) & 0xffu;
+}
+
+// Valid-row mask of a 16-row chunk whose first row has string index `lo`
+// against a string of `len` symbols (bit r set <=> 0 <= lo + r < len).
+__device__ __forceinline__ uint32_t chunk_valid_mask(int64_t lo, int64_t len) {
+    int64_t b = lo < 0 ? -lo : 0;
+    int64_t e = len - lo;
+    if (b > 16) b = 16;
+    if (e > 16) e = 16;
+    if (e <= b) return 0u;
+    return ((1u << e) - 1u) & ~((1u << b) - 1u);
+}
+
+__device__ __forceinline__ int warp_max(int v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(kFullMask, v, o));
+    return v;
+}
+
+__device__ __forceinline__ uint32_t lane_id() {
+    uint32_t l;
+    asm("mov.u32 %0, %%laneid;" : "=r"(l));
+    return l;
+}
+
+// gpu-scope release store / acquire load for inter-CTA flag protocols.
+__device__ __forceinline__ void st_release_gpu(uint32_t* p, uint32_t v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+}  // namespace wlcs

@@ -1,0 +1,115 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the oracle.
+
+Bit-exact for every length and every recovered subsequence (integer/byte
+work: no tolerance).  Mirrors the reference's own tests:
+proj/tests/test_core.cpp, test_kernels.cpp, test_parallel.cpp, acceptance.cpp.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+DNA = b"ACGT"
+PROTEIN = b"ACDEFGHIKLMNPQRSTVWY"
+CHILD_SEED_OFFSET = 0x9E3779B97F4A7C15  # include/wavelcs/bench.hpp:74
+
+
+def rand_pairs(rng, n, lo, hi, alphabet):
+    a = np.frombuffer(alphabet, dtype=np.uint8)
+    xs, ys = [], []
+    for _ in range(n):
+        m = int(rng.integers(lo, hi + 1))
+        k = int(rng.integers(lo, hi + 1))
+        xs.append(a[rng.integers(0, len(a), m)].tobytes())
+        ys.append(a[rng.integers(0, len(a), k)].tobytes())
+    return xs, ys
+
+
+def check_batch(wl, restatement, xs, ys):
+    xb, xo, yb, yo = wl.pack_pairs(xs, ys)
+    got = wl.lcs_length_batch(xb, xo, yb, yo)
+    want = restatement.length_batch(xb, xo, yb, yo)
+    bad = np.nonzero(got != want)[0]
+    assert bad.size == 0, f"{bad.size} mismatches, first pair {bad[0]}: got {got[bad[0]]} want {want[bad[0]]} (m={len(xs[bad[0]])}, n={len(ys[bad[0]])})"
+
+
+def test_golden_lengths(wl):
+    # proj/tests/test_core.cpp:58-62
+    assert wl.lcs_length(b"", b"") == 0
+    assert wl.lcs_length(b"ATGC", b"ATGC") == 4
+    assert wl.lcs_length(b"ABCBDAB", b"BDCABA") == 4
+    assert wl.lcs_length(b"", b"ATGC") == 0
+
+
+def test_golden_subsequences(wl):
+    # proj/tests/test_core.cpp:69-85, test_cli.cpp:82-91
+    assert wl.lcs_subsequence(b"ABCBDAB", b"BDCABA") == b"BDAB"
+    assert wl.lcs_subsequence(b"ATGC", b"ATGC") == b"ATGC"
+    assert wl.lcs_subsequence(b"ATGC", b"") == b""
+
+
+@pytest.mark.parametrize("alphabet", [DNA, PROTEIN])
+def test_batch_small_random(wl, restatement, alphabet):
+    rng = np.random.default_rng(1234)
+    xs, ys = rand_pairs(rng, 3000, 0, 300, alphabet)
+    check_batch(wl, restatement, xs, ys)
+
+
+def test_batch_c2_sample(wl, restatement):
+    rng = np.random.default_rng(77)
+    xs, ys = rand_pairs(rng, 4096, 200, 1000, PROTEIN)
+    check_batch(wl, restatement, xs, ys)
+
+
+def test_batch_edges(wl, restatement):
+    rng = np.random.default_rng(5)
+    a = np.arange(256, dtype=np.uint8)
+    xs = [b"", b"A", b"", b"AAAA", b"A" * 1000, b"ACGT" * 3000, bytes(a), bytes(a[::-1]) * 3]
+    ys = [b"", b"", b"A", b"AAAA", b"C" * 1000, b"TGCA" * 2500, bytes(a) * 2, bytes(a)]
+    # large alphabet (overflows a warp's match-mask slice) and very long pairs
+    for _ in range(40):
+        m, n = int(rng.integers(1, 3000)), int(rng.integers(1, 3000))
+        xs.append(a[rng.integers(0, 256, m)].tobytes())
+        ys.append(a[rng.integers(0, 256, n)].tobytes())
+    xs.append(rng.integers(0, 4, 20000).astype(np.uint8).tobytes())
+    ys.append(rng.integers(0, 4, 9000).astype(np.uint8).tobytes())
+    check_batch(wl, restatement, xs, ys)
+
+
+@pytest.mark.parametrize("m,n", [(1, 1), (5, 300), (300, 5), (1000, 1000), (4097, 33), (33, 4097),
+                                 (5000, 200), (12345, 6789)])
+def test_single_pair_lengths(wl, restatement, m, n):
+    rng = np.random.default_rng(m * 7919 + n)
+    x = rng.choice(np.frombuffer(DNA, np.uint8), m).tobytes()
+    y = rng.choice(np.frombuffer(DNA, np.uint8), n).tobytes()
+    assert wl.lcs_length(x, y) == restatement.length_bitpar(x, y)
+
+
+def test_c1_checkpoint(wl, restatement):
+    # generate_random(10000, "ACGT", 1) vs seed 1 + offset -> 6538
+    x = restatement.generate_random(10000, DNA, 1)
+    y = restatement.generate_random(10000, DNA, 1 + CHILD_SEED_OFFSET)
+    assert wl.lcs_length(x, y) == 6538
+    sub = wl.lcs_subsequence(x, y)
+    assert len(sub) == 6538
+    assert sub == restatement.subsequence_bitrows(x, y)
+
+
+@pytest.mark.parametrize("alphabet", [DNA, PROTEIN, b"AC"])
+def test_subsequence_random(wl, restatement, alphabet):
+    rng = np.random.default_rng(len(alphabet))
+    a = np.frombuffer(alphabet, np.uint8)
+    for _ in range(60):
+        m, n = int(rng.integers(0, 400)), int(rng.integers(0, 400))
+        x = a[rng.integers(0, len(a), m)].tobytes()
+        y = a[rng.integers(0, len(a), n)].tobytes()
+        assert wl.lcs_subsequence(x, y) == restatement.subsequence(x, y), (x, y)
+
+
+def test_capacity_semantics(wl):
+    # proj/tests/test_core.cpp:122-126
+    with pytest.raises(wl.CapacityError):
+        wl.lcs_length(b"ATGC", b"ATGC", 16)
+    assert wl.lcs_length(b"ATGC", b"ATGC", 1024) == 4
+    with pytest.raises(wl.CapacityError):
+        wl.lcs_length(b"", b"", 1)
