@@ -113,6 +113,16 @@ int wlcs_length_batch_device(const uint8_t* d_xs, const uint64_t* d_x_off, const
 int wlcs_length_device(const uint8_t* d_x, size_t m, const uint8_t* d_y, size_t n, int variant,
                        uint32_t* out, void* stream);
 
+/* Instrumentation for bench.py: when on, the batch entry points bracket their
+ * main kernel with CUDA events on the launching stream; wlcs_last_kernel_ms
+ * returns that kernel's duration (ms) for the calling thread's last batch. */
+int wlcs_set_timing(int on);
+int wlcs_last_kernel_ms(float* ms);
+
+/* Integer ALU-pipe peak of the current device (int32 ops/s, best of reps),
+ * measured by a LOP3 stream kernel: the roofline denominator of the fill. */
+int wlcs_probe_int_peak(int reps, double* ops_per_s);
+
 /* Page-locked host memory for zero-copy-speed transfers (cudaHostAlloc). */
 void* wlcs_host_alloc(size_t bytes);
 void wlcs_host_free(void* p);
@@ -122,6 +132,15 @@ void wlcs_host_free(void* p);
  * Synthetic-input helper for benchmarks and tests; host-only. */
 int wlcs_generate_random(size_t length, const uint8_t* alphabet, size_t alphabet_len,
                          uint64_t seed, uint8_t* out);
+
+/* Synthetic batch for benchmarks/tests (BASELINE config C2 procedure):
+ * master = std::mt19937_64(seed); per pair k: m = lo + master() % (hi-lo+1),
+ * n likewise, then seed_x = master(), seed_y = master() and
+ * x_k = generate_random(m, alphabet, seed_x), y_k = generate_random(n, ...).
+ * xs / ys must hold pairs*hi bytes; offsets pairs+1 entries. */
+int wlcs_generate_pairs(size_t pairs, size_t lo, size_t hi, const uint8_t* alphabet,
+                        size_t alphabet_len, uint64_t seed, uint8_t* xs, uint64_t* x_off,
+                        uint8_t* ys, uint64_t* y_off);
 
 #ifdef __cplusplus
 }

@@ -107,6 +107,11 @@ lib.wlcs_host_alloc.restype = _vp
 lib.wlcs_host_alloc.argtypes = [_sz]
 lib.wlcs_host_free.argtypes = [_vp]
 lib.wlcs_generate_random.argtypes = [_sz, _vp, _sz, ctypes.c_uint64, _vp]
+lib.wlcs_generate_pairs.argtypes = [_sz, _sz, _sz, _vp, _sz, ctypes.c_uint64, _vp, _u64p, _vp,
+                                    _u64p]
+lib.wlcs_set_timing.argtypes = [ctypes.c_int]
+lib.wlcs_last_kernel_ms.argtypes = [ctypes.POINTER(ctypes.c_float)]
+lib.wlcs_probe_int_peak.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_double)]
 
 
 def _check(rc: int) -> None:

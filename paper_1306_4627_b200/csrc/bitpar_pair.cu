@@ -140,6 +140,9 @@ __global__ void __launch_bounds__(32) pair_strip_kernel(PairDev d) {
         uint32_t cout = 0;
         StoreHook<K, STORE> hook{STORE ? d.rows_out + g * d.Mpad * K : nullptr, 0, d.rows};
         const int T = nchunks + 31;
+        // lane l works on chunk t - l: at t = 0 only lane 0 has a real chunk
+        uint32_t vm = (lane == 0 && nchunks > 0) ? chunk_valid_mask(-a_r, d.rows) : 0u;
+        uint4 cur = fetch_chunk(rstart, -int(lane), vm, d.row_lo, d.row_hi, d.safe16);
         for (int t = 0; t < T; ++t) {
             if (has_left && (t % kCarryBatch) == 0 && t < nchunks) {
                 const int need = min(t + kCarryBatch, nchunks);
@@ -152,24 +155,31 @@ __global__ void __launch_bounds__(32) pair_strip_kernel(PairDev d) {
                             ? __ldcg(left_carry + t + lane)
                             : 0u;
             }
+            const int ch = t - int(lane);
+            const int64_t lo = int64_t(ch) * 16 - a_r;
+            const uint32_t vm_next =
+                (ch + 1 >= 0 && ch + 1 < nchunks) ? chunk_valid_mask(lo + 16, d.rows) : 0u;
+            const uint4 nxt = fetch_chunk(rstart, ch + 1, vm_next, d.row_lo, d.row_hi, d.safe16);
             uint32_t cin = __shfl_up_sync(kFullMask, cout, 1);
             const uint32_t from_left = __shfl_sync(kFullMask, inbuf, t % kCarryBatch);
             if (lane == 0) cin = (has_left && t < nchunks) ? from_left : 0u;
             cin <<= 16;
             cout = 0;
-            const int ch = t - int(lane);
-            const int64_t lo = int64_t(ch) * 16 - a_r;
-            const bool full = ch >= 0 && lo >= 0 && lo + 16 <= d.rows;
-            const uint32_t vm = (ch >= 0 && ch < nchunks) ? chunk_valid_mask(lo, d.rows) : 0u;
             hook.lo = lo;
-            sweep_chunk<true, K>(__all_sync(kFullMask, full), V, map, pm, lane_off,
-                                 rstart + int64_t(ch) * 16, d.row_lo, d.row_hi, vm, cin, cout,
-                                 hook);
+            uint32_t off[16];
+            if (__all_sync(kFullMask, vm == 0xffffu)) {
+                chunk_offsets(cur, map, cs, lane_off, off);
+            } else {
+                chunk_offsets_masked(cur, vm, map, cs, lane_off, off);
+            }
+            rows16<true, K>(V, pm, off, vm, cin, cout, hook);
             if (has_right && lane == 31 && ch >= 0 && ch < nchunks) {
                 my_carry[ch] = cout;
                 if (((ch + 1) % kCarryBatch) == 0 || ch + 1 == nchunks)
                     st_release_gpu(d.progress + strip, uint32_t(ch + 1));
             }
+            cur = nxt;
+            vm = vm_next;
         }
         int zeros = lane_zero_count<K>(V, g * K, d.cols);
 #pragma unroll

@@ -75,6 +75,9 @@ struct DevBuf {
 
 struct Ctx {
     int device = 0;
+    bool timing = false;          // wlcs_set_timing: bracket the main kernel with events
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    float last_main_ms = -1.f;
     int sms = 148;
     cudaStream_t stream = nullptr;
     // batch
@@ -187,6 +190,7 @@ int pair_setup(Ctx& c, const uint8_t* d_row, int64_t rows, const uint8_t* row_lo
     uint32_t* sigma_dev = reinterpret_cast<uint32_t*>(sb + 1536);
     d.ticket = reinterpret_cast<uint32_t*>(sb + 1540);
     d.zeros = reinterpret_cast<unsigned long long*>(sb + 1544);
+    d.safe16 = reinterpret_cast<const uint4*>(sb + 2048);  // zeroed below
     int sigma = 0;
     WLCS_CUDA(wlcs::pair_prepare(d, present, map, sigma_dev, c.stream, &sigma));
     plan.K = choose_k(c, d.W, sigma, store);
@@ -204,6 +208,7 @@ int pair_setup(Ctx& c, const uint8_t* d_row, int64_t rows, const uint8_t* row_lo
     d.carry = reinterpret_cast<uint32_t*>(c.carry.as<uint8_t>() + prog_bytes);
     WLCS_CUDA(cudaMemsetAsync(d.progress, 0, prog_bytes, c.stream));
     WLCS_CUDA(cudaMemsetAsync(d.ticket, 0, 4 + 4 + 8, c.stream));
+    WLCS_CUDA(cudaMemsetAsync(sb + 2048, 0, 16, c.stream));
     d.Mpad = (rows + 15) & ~int64_t(15);
     d.rows_out = nullptr;
     if (store) {
@@ -259,12 +264,18 @@ int batch_device(Ctx& c, const uint8_t* d_xs, const uint64_t* d_xoff, const uint
     d.out = d_out;
     d.pairs = uint32_t(pairs);
     d.pm_bytes = env_int("WLCS_BATCH_PM_KB", 24) * 1024;
-    WLCS_CUDA(wlcs::batch_launch(d, c.ws.p, cub_bytes, c.sms, stream));
+    if (c.timing && !c.ev0) {
+        WLCS_CUDA(cudaEventCreate(&c.ev0));
+        WLCS_CUDA(cudaEventCreate(&c.ev1));
+    }
+    WLCS_CUDA(wlcs::batch_launch(d, c.ws.p, cub_bytes, c.sms, stream, c.timing ? c.ev0 : nullptr,
+                                 c.timing ? c.ev1 : nullptr));
     uint32_t overflow = 0;
     WLCS_CUDA(cudaMemcpyAsync(&overflow,
                               wlcs::batch_overflow_count_ptr(c.ws.p, cub_bytes, uint32_t(pairs)),
                               4, cudaMemcpyDeviceToHost, stream));
     WLCS_CUDA(cudaStreamSynchronize(stream));
+    if (c.timing) WLCS_CUDA(cudaEventElapsedTime(&c.last_main_ms, c.ev0, c.ev1));
     if (overflow == 0) return WLCS_OK;
     // Pairs too long or with too large an alphabet for one warp: strip kernel.
     std::vector<uint32_t> ids(overflow);
@@ -445,6 +456,55 @@ int wlcs_length_batch_ex(const uint8_t* xs, const uint64_t* x_off, const uint8_t
 int wlcs_length_batch(const uint8_t* xs, const uint64_t* x_off, const uint8_t* ys,
                       const uint64_t* y_off, size_t pairs, uint32_t* out) {
     return wlcs_length_batch_ex(xs, x_off, ys, y_off, pairs, WLCS_VARIANT_BITPARALLEL, out);
+}
+
+int wlcs_set_timing(int on) {
+    Ctx* c = nullptr;
+    int rc = get_ctx(&c);
+    if (rc) return rc;
+    c->timing = on != 0;
+    c->last_main_ms = -1.f;
+    return WLCS_OK;
+}
+
+int wlcs_last_kernel_ms(float* ms) {
+    Ctx* c = nullptr;
+    int rc = get_ctx(&c);
+    if (rc) return rc;
+    *ms = c->last_main_ms;
+    return WLCS_OK;
+}
+
+int wlcs_probe_int_peak(int reps, double* ops_per_s) {
+    Ctx* c = nullptr;
+    int rc = get_ctx(&c);
+    if (rc) return rc;
+    WLCS_CUDA(c->small.ensure(4096));
+    WLCS_CUDA(wlcs::int_peak_probe(reps, ops_per_s, c->small.as<uint32_t>() + 900));
+    return WLCS_OK;
+}
+
+int wlcs_generate_pairs(size_t pairs, size_t lo, size_t hi, const uint8_t* alphabet,
+                        size_t alphabet_len, uint64_t seed, uint8_t* xs, uint64_t* x_off,
+                        uint8_t* ys, uint64_t* y_off) {
+    if (alphabet_len == 0 || !alphabet || hi < lo)
+        return fail(WLCS_E_INVALID_ARGUMENT, "generate_pairs: bad alphabet or length range");
+    std::mt19937_64 master(seed);
+    uint64_t xo = 0, yo = 0;
+    x_off[0] = y_off[0] = 0;
+    for (size_t k = 0; k < pairs; ++k) {
+        const size_t m = lo + size_t(master() % (hi - lo + 1));
+        const size_t n = lo + size_t(master() % (hi - lo + 1));
+        const uint64_t sx = master(), sy = master();
+        std::mt19937_64 rx(sx), ry(sy);
+        for (size_t i = 0; i < m; ++i) xs[xo + i] = alphabet[rx() % alphabet_len];
+        for (size_t j = 0; j < n; ++j) ys[yo + j] = alphabet[ry() % alphabet_len];
+        xo += m;
+        yo += n;
+        x_off[k + 1] = xo;
+        y_off[k + 1] = yo;
+    }
+    return WLCS_OK;
 }
 
 void* wlcs_host_alloc(size_t bytes) {

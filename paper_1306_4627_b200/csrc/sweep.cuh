@@ -72,36 +72,70 @@ struct NoRowHook {
     __device__ __forceinline__ void operator()(int, bool, const uint32_t*) const {}
 };
 
-// Process the 16 rows of one chunk.  `full` = all 16 rows valid for every
-// lane of the warp (warp-uniform): the fast path is fully unrolled; the
-// masked path treats invalid rows as identity rows (code 0 = zero masks).
-// hook(r, valid, V) runs after each row (used to store bit rows).
-// MapT is uint8_t (batch: <= 255 codes) or uint16_t (single pair: up to 257).
-template <bool CHAIN, int K, typename MapT, typename Hook>
-__device__ __forceinline__ void sweep_chunk(bool full, uint32_t* V, const MapT* map,
-                                            const uint8_t* pm, uint32_t lane_off,
-                                            const uint8_t* chunk_ptr, const uint8_t* alloc_lo,
-                                            const uint8_t* alloc_hi, uint32_t vm, uint32_t& cin,
-                                            uint32_t& cout, const Hook& hook) {
-    constexpr uint32_t cs = PmLayout<K>::code_stride;
-    if (full) {
-        const uint4 c = __ldg(reinterpret_cast<const uint4*>(chunk_ptr));
+// A step processes the 16 rows of one chunk in two parts so that only the
+// small part has a masked variant (keeps the hot code small for the I-cache):
+//  (a) offsets: off[r] = PM byte offset of row r's match masks for this lane
+//      (code * code_stride + lane_off; code 0 = all-zero masks = identity row)
+//  (b) rows:    16 unrolled row updates reading P from off[r].
+template <typename MapT>
+__device__ __forceinline__ void chunk_offsets(const uint4& c, const MapT* map, uint32_t cs,
+                                              uint32_t lane_off, uint32_t* off) {
 #pragma unroll
-        for (int r = 0; r < 16; ++r) {
-            const uint32_t code = map[chunk_byte(c, r)];
-            row_update<CHAIN, K>(V, pm, code * cs + lane_off, cin, cout);
-            hook(r, true, V);
-        }
-    } else {
-        const uint4 c = vm ? load_chunk16(chunk_ptr, alloc_lo, alloc_hi) : make_uint4(0, 0, 0, 0);
-#pragma unroll 1
-        for (int r = 0; r < 16; ++r) {
-            const bool valid = (vm >> r) & 1u;
-            const uint32_t code = valid ? uint32_t(map[chunk_byte(c, r)]) : 0u;
-            row_update<CHAIN, K>(V, pm, code * cs + lane_off, cin, cout);
-            hook(r, valid, V);
-        }
+    for (int r = 0; r < 16; ++r) off[r] = uint32_t(map[chunk_byte(c, r)]) * cs + lane_off;
+}
+
+// Rows whose bit in vm is clear become identity rows.
+template <typename MapT>
+__device__ __forceinline__ void chunk_offsets_masked(const uint4& c, uint32_t vm, const MapT* map,
+                                                     uint32_t cs, uint32_t lane_off,
+                                                     uint32_t* off) {
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+        const uint32_t code = ((vm >> r) & 1u) ? uint32_t(map[chunk_byte(c, r)]) : 0u;
+        off[r] = code * cs + lane_off;
     }
+}
+
+// Replaces the bytes of invalid rows by `zrep` (a byte value absent from the
+// task's column alphabet, replicated x4) so that they map to code 0.
+__device__ __forceinline__ uint4 sanitize_chunk(uint4 c, uint32_t vm, uint32_t zrep) {
+    uint32_t w[4] = {c.x, c.y, c.z, c.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const uint32_t m4 = (vm >> (4 * i)) & 0xfu;
+        const uint32_t keep = ((m4 * 0x00204081u) & 0x01010101u) * 0xffu;  // bit b -> byte b
+        w[i] = (w[i] & keep) | (zrep & ~keep);
+    }
+    return make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+
+// hook(r, valid, V) runs after each row (used to store bit rows).
+template <bool CHAIN, int K, typename Hook>
+__device__ __forceinline__ void rows16(uint32_t* V, const uint8_t* pm, const uint32_t* off,
+                                       uint32_t vm, uint32_t& cin, uint32_t& cout,
+                                       const Hook& hook) {
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+        row_update<CHAIN, K>(V, pm, off[r], cin, cout);
+        hook(r, ((vm >> r) & 1u) != 0u, V);
+    }
+}
+
+// The 16-byte chunk `ch` of a lane's row string (chunk addresses are 16-byte
+// aligned by construction).  The common case is one unconditional LDG.128 the
+// compiler can hoist a whole step ahead of its use; straddling chunks take a
+// warp-uniform slow path.
+__device__ __forceinline__ uint4 fetch_chunk(const uint8_t* rstart, int ch, uint32_t vm,
+                                             const uint8_t* alloc_lo, const uint8_t* alloc_hi,
+                                             const uint4* safe) {
+    const uint8_t* p = rstart + int64_t(ch) * 16;
+    bool slow;
+    uint4 c = fetch_chunk_fast(p, vm, alloc_lo, alloc_hi, safe, slow);
+    if (__any_sync(kFullMask, slow)) {
+        if (slow) c = load_chunk16(p, alloc_lo, alloc_hi);
+    }
+    return c;
 }
 
 // Zero bits of the lane's K words below global column `cols`; `word0` is the

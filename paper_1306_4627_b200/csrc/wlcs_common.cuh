@@ -35,9 +35,11 @@ __device__ __forceinline__ uint4 load_chunk16(const uint8_t* p, const uint8_t* a
     return make_uint4(w[0], w[1], w[2], w[3]);
 }
 
+// Byte r (0..15) of a 16-byte chunk; r is a compile-time constant in the
+// unrolled sweeps, so this is one PRMT.
 __device__ __forceinline__ uint32_t chunk_byte(const uint4& c, int r) {
     const uint32_t w = (r < 4) ? c.x : (r < 8) ? c.y : (r < 12) ? c.z : c.w;
-    return (w >> (8 * (r & 3))) & 0xffu;
+    return __byte_perm(w, 0u, 0x4440u | uint32_t(r & 3));
 }
 
 // Valid-row mask of a 16-row chunk whose first row has string index `lo`
@@ -49,6 +51,30 @@ __device__ __forceinline__ uint32_t chunk_valid_mask(int64_t lo, int64_t len) {
     if (e > 16) e = 16;
     if (e <= b) return 0u;
     return ((1u << e) - 1u) & ~((1u << b) - 1u);
+}
+
+// 32-bit variant for in-warp ranges (lo may be negative).
+__device__ __forceinline__ uint32_t valid_mask16(int lo, int len) {
+    int b = -lo;
+    b = b < 0 ? 0 : (b > 16 ? 16 : b);
+    int e = len - lo;
+    e = e < 0 ? 0 : (e > 16 ? 16 : e);
+    return e <= b ? 0u : ((1u << e) - 1u) & ~((1u << b) - 1u);
+}
+
+// One unconditional, hoistable 16-byte load for a chunk that holds valid
+// bytes (vm != 0) and lies inside [alloc_lo, alloc_hi); any other chunk
+// reads the 16-byte zero block `safe` instead.  `slow` flags chunks that hold
+// valid bytes but straddle the allocation end: the caller re-reads those with
+// load_chunk16 (rare: only the last string of a buffer).
+__device__ __forceinline__ uint4 fetch_chunk_fast(const uint8_t* p, uint32_t vm,
+                                                  const uint8_t* alloc_lo,
+                                                  const uint8_t* alloc_hi, const uint4* safe,
+                                                  bool& slow) {
+    const bool inb = p >= alloc_lo && p + 16 <= alloc_hi;
+    slow = vm != 0u && !inb;
+    const uint4* src = (vm != 0u && inb) ? reinterpret_cast<const uint4*>(p) : safe;
+    return __ldg(src);
 }
 
 __device__ __forceinline__ int warp_max(int v) {

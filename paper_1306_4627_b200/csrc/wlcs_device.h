@@ -26,12 +26,15 @@ struct BatchDev {
     uint32_t* vals;
     uint32_t* meta;
     uint32_t* overflow;
+    const uint4* safe16;   // 16 zero bytes in device memory
 };
 
 size_t batch_workspace_bytes(uint32_t pairs, size_t* cub_bytes);
 int batch_smem_per_cta(int pm_bytes);
 cudaError_t batch_launch(BatchDev d, void* workspace, size_t cub_bytes, int sms,
-                         cudaStream_t stream);
+                         cudaStream_t stream, cudaEvent_t ev_main0 = nullptr,
+                         cudaEvent_t ev_main1 = nullptr);
+cudaError_t int_peak_probe(int reps, double* ops_per_s, uint32_t* scratch);
 uint32_t* batch_overflow_count_ptr(void* workspace, size_t cub_bytes, uint32_t pairs);
 uint32_t* batch_overflow_list_ptr(void* workspace, size_t cub_bytes, uint32_t pairs);
 
@@ -59,6 +62,7 @@ struct PairDev {
     unsigned long long* zeros;  // LCS accumulator
     uint32_t* rows_out;     // optional: bit rows [G][Mpad][K]
     int64_t Mpad;
+    const uint4* safe16;    // 16 zero bytes in device memory
 };
 
 cudaError_t pair_prepare(PairDev& d, uint32_t* present256, uint16_t* map256, uint32_t* sigma_dev,
