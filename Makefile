@@ -4,16 +4,17 @@
 NVCC ?= /usr/local/cuda/bin/nvcc
 CXX ?= g++
 ARCH := -gencode arch=compute_100a,code=sm_100a
-NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Iinclude -Xcompiler -fPIC -Xcompiler -Wall
 SRC := paper_1306_4627_b200/csrc
 OBJ := build/obj
 LIB := paper_1306_4627_b200/_lib/libwavelcs_b200.so
+FACADE_TEST := tests/cpp/test_facade
 CU_SRCS := $(wildcard $(SRC)/*.cu)
 CXX_SRCS := $(wildcard $(SRC)/*.cpp)
 OBJS := $(patsubst $(SRC)/%.cu,$(OBJ)/%.o,$(CU_SRCS)) $(patsubst $(SRC)/%.cpp,$(OBJ)/%.cpp.o,$(CXX_SRCS))
 HDRS := $(wildcard $(SRC)/*.cuh) $(wildcard $(SRC)/*.h) $(wildcard include/*.h) $(wildcard include/*.hpp)
 
-all: lib oracle
+all: lib oracle $(FACADE_TEST)
 
 lib: $(LIB)
 
@@ -26,7 +27,14 @@ $(OBJ)/%.o: $(SRC)/%.cu $(HDRS) $(SRC)/rowstep.cuh
 
 $(OBJ)/%.cpp.o: $(SRC)/%.cpp $(HDRS)
 	@mkdir -p $(OBJ)
-	$(CXX) -std=c++17 -O2 -fPIC -Wall -Wextra -Iinclude -c $< -o $@
+	$(CXX) -std=c++20 -O2 -fPIC -Wall -Wextra -Iinclude -c $< -o $@
+
+# C++ facade test (the reference's unit cases against wavelcs_b200.hpp);
+# lives in tests/ so it travels to the GPU box with the snapshot.
+$(FACADE_TEST): tests/cpp/test_facade.cpp $(LIB) include/wavelcs_b200.hpp
+	$(CXX) -std=c++20 -O2 -Wall -Wextra -Iinclude -o $@ $< -L$(dir $(LIB)) -lwavelcs_b200 \
+	    -Wl,-rpath,'$$ORIGIN/../../$(dir $(LIB))'
+
 
 $(LIB): $(OBJS)
 	@mkdir -p $(dir $@)
@@ -36,6 +44,6 @@ oracle:
 	$(MAKE) -s -C oracle
 
 clean:
-	rm -rf build $(LIB)
+	rm -rf build $(LIB) $(FACADE_TEST)
 
 .PHONY: all lib oracle clean

@@ -395,27 +395,14 @@ def run_pair_config(args, dist):
     """C1/C3 (length + subsequence) and C4/C5 (length only), single GPU."""
     import torch
     import paper_1306_4627_b200 as wl
+    from paper_1306_4627_b200 import workloads
     torch.cuda.set_device(dist.local_rank)
-    rng_seed = args.seed
-    if args.config == "c1":
-        x = wl.generate_random(10000, DNA, 1)
-        y = wl.generate_random(10000, DNA, 1 + CHILD_SEED_OFFSET)
-        sub = True
-        name = "C1: 10k x 10k DNA, length + subsequence"
-    elif args.config == "c3":
-        x = wl.generate_random(100000, DNA, rng_seed)
-        y = mutate(x, rng_seed + 1)
-        sub = True
-        name = "C3: 100k x ~100k mutated DNA, length + subsequence"
-    elif args.config == "c4":
-        x = wl.generate_random(1000000, DNA, rng_seed)
-        y = wl.generate_random(1000000, DNA, rng_seed + CHILD_SEED_OFFSET)
-        sub = False
-        name = "C4: 1M x 1M DNA, length only"
-    else:
-        x, y = zipf_bytes(2000000, rng_seed), zipf_bytes(500000, rng_seed + 1)
-        sub = False
-        name = "C5: 2M x 500k Zipf(1.1) bytes, length only"
+    x, y = workloads.config_pair(args.config, args.seed)
+    sub = args.config in ("c1", "c3")
+    name = {"c1": "C1: 10k x 10k DNA, length + subsequence",
+            "c3": "C3: 100k x ~100k mutated DNA, length + subsequence",
+            "c4": "C4: 1M x 1M DNA, length only",
+            "c5": "C5: 2M x 500k Zipf(1.1) bytes, length only"}[args.config]
     cells = len(x) * len(y)
     fn = (lambda: wl.lcs_subsequence(x, y, wl.NO_BUDGET)) if sub else \
         (lambda: wl.lcs_length(x, y, wl.NO_BUDGET))
@@ -433,40 +420,10 @@ def run_pair_config(args, dist):
     return {"metric": METRIC, "value": round(cells / t / 1e9, 3), "unit": UNIT, "n_gpus": 1,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t * 1e3, 3),
             "higher_is_better": True, "scaling": "none", "vs_baseline": None, "dtype": "u32",
-            "data": "synthetic", "config": {"workload": name, "lcs_length": length},
+            "data": "synthetic (paper_1306_4627_b200/workloads.py)",
+            "config": {"workload": name, "lcs_length": length, "m": len(x), "n": len(y)},
             "clocks": clocks.summary(),
             "note": "end-to-end wall time through the C-ABI (H2D, fill, traceback, D2H)"}
-
-
-def mutate(x: bytes, seed: int) -> bytes:
-    """C3 mutation rule: one uniform draw u per source symbol:
-    u < 0.10 substitute by one of the 3 other bases, u < 0.12 delete,
-    u < 0.14 insert a uniform base then copy, else copy."""
-    rng = np.random.Generator(np.random.MT19937(seed))
-    u = rng.random(len(x))
-    sub = rng.integers(1, 4, len(x))
-    ins = rng.integers(0, 4, len(x))
-    code = {c: i for i, c in enumerate(DNA)}
-    out = bytearray()
-    for k, c in enumerate(x):
-        if u[k] < 0.10:
-            out.append(DNA[(code[c] + int(sub[k])) % 4])
-        elif u[k] < 0.12:
-            continue
-        elif u[k] < 0.14:
-            out.append(DNA[int(ins[k])])
-            out.append(c)
-        else:
-            out.append(c)
-    return bytes(out)
-
-
-def zipf_bytes(n: int, seed: int, s: float = 1.1) -> bytes:
-    """C5 symbols: Zipf(s) over 256 ranks by inverse CDF; rank k -> byte k-1."""
-    rng = np.random.Generator(np.random.MT19937(seed))
-    w = 1.0 / np.arange(1, 257) ** s
-    cdf = np.cumsum(w / w.sum())
-    return np.searchsorted(cdf, rng.random(n)).astype(np.uint8).tobytes()
 
 
 def main():

@@ -1,0 +1,95 @@
+// wavelcs_b200.hpp -- C++ drop-in facade for the reference "wavelcs" LCS
+// entry points, backed by the B200 library through the C-ABI
+// (include/wavelcs_capi.h).  Same namespace, names, argument meaning and
+// exception types as the reference headers (paths under /root/reference/proj):
+//
+//   Length lcs_length(x, y, memory_budget)     include/wavelcs/serial.hpp:24-25
+//   check_capacity(m, n, budget)               include/wavelcs/tables.hpp:16
+//   class Sequence, is_subsequence             include/wavelcs/sequence.hpp:13-38
+//   CapacityError / ConfigError / InputError /
+//   EquivalenceError                           include/wavelcs/errors.hpp:8-30
+//   generate_random(length, alphabet, seed)    include/wavelcs/io.hpp:34
+//
+// plus the single-call subsequence that replaces the composition
+//   traceback(lcs_fill_parallel(x, y, cfg).back, x, M, N)
+// (tools/wavelcs_main.cpp:78-86; serial.hpp:30; parallel.hpp:92-93) and a
+// batch entry point.  Link against paper_1306_4627_b200/_lib/libwavelcs_b200.so.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <string_view>
+#include <utility>
+#include <vector>
+
+namespace wavelcs {
+
+using Length = std::uint32_t;
+
+inline constexpr std::size_t kDefaultMemoryBudget = std::size_t{2} * 1024 * 1024 * 1024;
+inline constexpr std::size_t kNoMemoryBudget = ~std::size_t{0};
+
+class CapacityError : public std::runtime_error {
+public:
+    using std::runtime_error::runtime_error;
+};
+class ConfigError : public std::runtime_error {
+public:
+    using std::runtime_error::runtime_error;
+};
+class InputError : public std::runtime_error {
+public:
+    using std::runtime_error::runtime_error;
+};
+class EquivalenceError : public std::logic_error {
+public:
+    using std::logic_error::logic_error;
+};
+/// CUDA failure inside the library (no reference counterpart: the reference
+/// never leaves the CPU).  There is no CPU fallback.
+class DeviceError : public std::runtime_error {
+public:
+    using std::runtime_error::runtime_error;
+};
+
+class Sequence {
+public:
+    Sequence() = default;
+    explicit Sequence(std::string symbols) : symbols_(std::move(symbols)) {}
+    std::size_t size() const noexcept { return symbols_.size(); }
+    bool empty() const noexcept { return symbols_.empty(); }
+    char operator[](std::size_t pos) const { return symbols_[pos]; }
+    const char* data() const noexcept { return symbols_.data(); }
+    std::string_view view() const noexcept { return symbols_; }
+    const std::string& str() const noexcept { return symbols_; }
+    void push_back(char symbol) { symbols_.push_back(symbol); }
+    auto begin() const noexcept { return symbols_.begin(); }
+    auto end() const noexcept { return symbols_.end(); }
+    friend bool operator==(const Sequence&, const Sequence&) = default;
+
+private:
+    std::string symbols_;
+};
+
+bool is_subsequence(const Sequence& candidate, const Sequence& text) noexcept;
+
+void check_capacity(std::size_t m, std::size_t n, std::size_t budget = kDefaultMemoryBudget);
+
+/// LCS length on the GPU.  Throws CapacityError exactly when the reference's
+/// tables would exceed memory_budget (the device path itself is O(M+N)).
+Length lcs_length(const Sequence& x, const Sequence& y,
+                  std::size_t memory_budget = kDefaultMemoryBudget);
+
+/// The reference's recovered subsequence (LEFT tie-break), in one call.
+Sequence lcs_subsequence(const Sequence& x, const Sequence& y,
+                         std::size_t memory_budget = kDefaultMemoryBudget);
+
+/// Lengths of many independent pairs (xs[k], ys[k]).
+std::vector<Length> lcs_length_batch(const std::vector<Sequence>& xs,
+                                     const std::vector<Sequence>& ys);
+
+Sequence generate_random(std::size_t length, const Sequence& alphabet, std::uint64_t seed);
+
+}  // namespace wavelcs

@@ -76,6 +76,10 @@ class Restatement:
         lib.orc_capacity_exceeded.argtypes = [ctypes.c_uint64] * 3
         lib.orc_generate_random.restype = None
         lib.orc_generate_random.argtypes = [_sz, _u8p, _sz, ctypes.c_uint64, _u8p]
+        lib.orc_strip_rows.restype = None
+        lib.orc_strip_rows.argtypes = [_u8p, _sz, _u8p, _sz, _u64p, _u8p, _u8p]
+        lib.orc_strip_zeros.restype = ctypes.c_uint64
+        lib.orc_strip_zeros.argtypes = [_u64p, _sz]
         lib.orc_length_batch.restype = None
         lib.orc_length_batch.argtypes = [_u8p, _u64p, _u8p, _u64p, _sz, _u32p]
         self.lib = lib
@@ -141,6 +145,21 @@ class Restatement:
         out = np.empty(max(1, length), dtype=np.uint8)
         self.lib.orc_generate_random(length, ap, alen, seed & (2**64 - 1), out.ctypes.data_as(_u8p))
         return out[:length].tobytes()
+
+    def strip_rows(self, x, ystrip, V: np.ndarray, carry_in: np.ndarray | None):
+        """Rows of x over one column strip; V (uint64, ceil(ns/64)) updated in
+        place; returns the per-row carry-out (uint8)."""
+        xa, xp, m = _buf(x)
+        ya, yp, ns = _buf(ystrip)
+        cout = np.zeros(max(1, m), np.uint8)
+        cin = None if carry_in is None else np.ascontiguousarray(carry_in, np.uint8)
+        self.lib.orc_strip_rows(xp, m, yp, ns, V.ctypes.data_as(_u64p),
+                                None if cin is None else cin.ctypes.data_as(_u8p),
+                                cout.ctypes.data_as(_u8p))
+        return cout[:m]
+
+    def strip_zeros(self, V: np.ndarray, ns: int) -> int:
+        return int(self.lib.orc_strip_zeros(V.ctypes.data_as(_u64p), ns))
 
     def length_batch(self, xs: np.ndarray, xoff: np.ndarray, ys: np.ndarray,
                      yoff: np.ndarray) -> np.ndarray:

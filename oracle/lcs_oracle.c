@@ -89,7 +89,7 @@ void orc_fill_tables(const uint8_t* x, size_t m, const uint8_t* y, size_t n, uin
                      uint8_t* back) {
     const size_t cs = n + 1;
     memset(dp, 0, (m + 1) * cs * sizeof(uint32_t));
-    if (m * n) memset(back, ARROW_LEFT, m * n);
+    if (m * n != 0) memset(back, ARROW_LEFT, m * n);
     for (size_t i = 1; i <= m; ++i) {
         uint32_t* cur = dp + i * cs;
         const uint32_t* prv = cur - cs;
@@ -318,3 +318,41 @@ void orc_generate_random(size_t length, const uint8_t* alphabet, size_t alen, ui
     mt64_seed(&s, seed);
     for (size_t k = 0; k < length; ++k) out[k] = alphabet[mt64_next(&s) % alen];
 }
+
+/* ---------------------------------------------------------------------
+ * Column-strip decomposition (the multi-GPU / multi-warp interface):
+ * rows [0, rows) of the bit-parallel fill restricted to columns
+ * [c0, c0 + ns) of y, with the strip's bit vector V (ceil(ns/64) words)
+ * carried across calls, carry_in[i] (0/1) injected into the strip's lowest
+ * column for row i and carry_out[i] = the carry leaving column c0+ns-1.
+ * ns must be a multiple of 64 except for the rightmost strip, so that the
+ * carry out of the last word is the carry out of the strip.  Chaining the
+ * strips left to right reproduces the whole-row fill (SURVEY.md section 7,
+ * "decompositions verified exact").
+ * ------------------------------------------------------------------- */
+void orc_strip_rows(const uint8_t* x, size_t rows, const uint8_t* ystrip, size_t ns,
+                    uint64_t* V, const uint8_t* carry_in, uint8_t* carry_out) {
+    const size_t words = (ns + 63) >> 6;
+    uint64_t* pm = (uint64_t*)malloc(256 * (words ? words : 1) * sizeof(uint64_t));
+    if (!pm) return;
+    build_pm64(ystrip, ns, words, pm);
+    for (size_t i = 0; i < rows; ++i) {
+        const uint64_t* P = pm + (size_t)x[i] * words;
+        unsigned carry = carry_in ? carry_in[i] : 0u;
+        for (size_t w = 0; w < words; ++w) {
+            const uint64_t v = V[w];
+            const uint64_t u = v & P[w];
+            const uint64_t s1 = v + u;
+            const unsigned c1 = s1 < v;
+            const uint64_t s = s1 + carry;
+            const unsigned c2 = s < s1;
+            carry = c1 | c2;
+            V[w] = s | (v & ~P[w]);
+        }
+        if (carry_out) carry_out[i] = (uint8_t)carry;
+    }
+    free(pm);
+}
+
+/* zero bits of V below ns (the strip's contribution to the LCS length) */
+uint64_t orc_strip_zeros(const uint64_t* V, size_t ns) { return zeros_in_prefix(V, ns); }

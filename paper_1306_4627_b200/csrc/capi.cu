@@ -13,7 +13,7 @@
 #include <unordered_map>
 #include <vector>
 
-#include "../../include/wavelcs_capi.h"
+#include "wavelcs_capi.h"
 #include "wlcs_device.h"
 
 namespace {

@@ -113,3 +113,105 @@ def test_capacity_semantics(wl):
     assert wl.lcs_length(b"ATGC", b"ATGC", 1024) == 4
     with pytest.raises(wl.CapacityError):
         wl.lcs_length(b"", b"", 1)
+
+
+# ---------------------------------------------------------------- fixtures
+import gzip  # noqa: E402
+import json  # noqa: E402
+import os  # noqa: E402
+import subprocess  # noqa: E402
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def test_golden_small_pairs_reference_tracebacks(wl):
+    """300 pairs whose lengths and tracebacks came from the reference itself."""
+    data = json.load(open(os.path.join(GOLDEN, "small_pairs.json")))
+    xs = [bytes.fromhex(c["x"]) for c in data["cases"]]
+    ys = [bytes.fromhex(c["y"]) for c in data["cases"]]
+    xb, xo, yb, yo = wl.pack_pairs(xs, ys)
+    got = wl.lcs_length_batch(xb, xo, yb, yo)
+    assert got.tolist() == [c["length"] for c in data["cases"]]
+    for x, y, c in zip(xs, ys, data["cases"]):
+        assert wl.lcs_length(x, y) == c["length"]
+        assert wl.lcs_subsequence(x, y).hex() == c["subsequence"]
+
+
+def test_golden_c1_subsequence(wl):
+    data = json.load(open(os.path.join(GOLDEN, "c1.json")))
+    from paper_1306_4627_b200 import workloads
+    x, y = workloads.config_pair("c1")
+    assert wl.lcs_subsequence(x, y).decode() == data["subsequence"]
+
+
+def test_golden_c2_sample(wl):
+    import ctypes
+    data = json.load(open(os.path.join(GOLDEN, "c2_sample.json")))
+    pairs = 512
+    xs = np.empty(pairs * 1000, np.uint8)
+    ys = np.empty(pairs * 1000, np.uint8)
+    xo = np.empty(pairs + 1, np.uint64)
+    yo = np.empty(pairs + 1, np.uint64)
+    a = np.frombuffer(PROTEIN, np.uint8)
+    wl._check(wl.lib.wlcs_generate_pairs(pairs, 200, 1000, a.ctypes.data, len(a), 20130619,
+                                         xs.ctypes.data,
+                                         xo.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)),
+                                         ys.ctypes.data,
+                                         yo.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64))))
+    got = wl.lcs_length_batch(xs[: int(xo[-1])], xo, ys[: int(yo[-1])], yo)
+    assert got.tolist() == data["lengths"]
+
+
+def test_golden_c3_reference_subsequence(wl):
+    """Config C3 (100k x ~100k mutated DNA): the recovered string must equal
+    the reference's own traceback (fixture generated by oracle/_ref)."""
+    data = json.load(gzip.open(os.path.join(GOLDEN, "c3.json.gz"), "rt"))
+    from paper_1306_4627_b200 import workloads
+    x, y = workloads.config_pair("c3")
+    assert wl.lcs_length(x, y, wl.NO_BUDGET) == data["length"]
+    sub = wl.lcs_subsequence(x, y, wl.NO_BUDGET)
+    assert len(sub) == data["length"]
+    assert sub.decode() == data["subsequence"]
+
+
+def test_batch_device_entry_point(wl, restatement):
+    import torch
+    rng = np.random.default_rng(21)
+    xs, ys = rand_pairs(rng, 1000, 0, 700, PROTEIN)
+    xb, xo, yb, yo = wl.pack_pairs(xs, ys)
+    dev = torch.device("cuda", 0)
+    d_xs = torch.from_numpy(np.concatenate([xb, np.zeros(16, np.uint8)])).to(dev)
+    d_ys = torch.from_numpy(np.concatenate([yb, np.zeros(16, np.uint8)])).to(dev)
+    d_xo = torch.from_numpy(xo.view(np.int64)).to(dev)
+    d_yo = torch.from_numpy(yo.view(np.int64)).to(dev)
+    d_out = torch.zeros(1000, dtype=torch.int32, device=dev)
+    wl.lcs_length_batch_device(d_xs.data_ptr(), d_xo.data_ptr(), d_ys.data_ptr(), d_yo.data_ptr(),
+                               1000, int(xo[-1]), int(yo[-1]), d_out.data_ptr(),
+                               torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert np.array_equal(d_out.cpu().numpy().astype(np.uint32),
+                          restatement.length_batch(xb, xo, yb, yo))
+
+
+@pytest.mark.parametrize("name", ["c4", "c5"])
+def test_large_configs_properties(wl, restatement, name):
+    """C4 (1M x 1M DNA) and C5 (2M x 500k Zipf bytes) at full size through
+    size-independent properties, plus a 200k prefix against the oracle."""
+    from paper_1306_4627_b200 import workloads
+    x, y = workloads.config_pair(name)
+    L = wl.lcs_length(x, y, wl.NO_BUDGET)
+    assert 0 < L <= min(len(x), len(y))
+    assert wl.lcs_length(y, x, wl.NO_BUDGET) == L                  # symmetry
+    c = x[-1:]
+    assert wl.lcs_length(x + c, y + c, wl.NO_BUDGET) == L + 1      # append (acceptance 4)
+    px, py = x[:200000], y[:150000]
+    assert wl.lcs_length(px, py, wl.NO_BUDGET) == restatement.length_bitpar(px, py)
+
+
+def test_cpp_facade_reference_unit_cases():
+    """The reference's unit cases against the C++ facade (tests/cpp)."""
+    exe = os.path.join(os.path.dirname(os.path.abspath(__file__)), "cpp", "test_facade")
+    assert os.path.exists(exe), "build() must produce tests/cpp/test_facade"
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "PASS" in r.stdout
