@@ -104,12 +104,14 @@ int wlcs_length_batch_ex(const uint8_t* xs, const uint64_t* x_off, const uint8_t
 /* Batch on DEVICE pointers already resident in HBM (current device), enqueued
  * on `stream` (a cudaStream_t, NULL = the library's per-thread stream).  The
  * call returns after the results are written to d_out (it synchronises the
- * stream once to collect pairs that need the single-pair path). */
+ * stream once to collect pairs that need the single-pair path).  d_xs and
+ * d_ys must be 16-byte aligned (cudaMalloc / torch allocations are). */
 int wlcs_length_batch_device(const uint8_t* d_xs, const uint64_t* d_x_off, const uint8_t* d_ys,
                              const uint64_t* d_y_off, size_t pairs, uint64_t xs_bytes,
                              uint64_t ys_bytes, int variant, uint32_t* d_out, void* stream);
 
-/* Single pair on DEVICE pointers (length only; budget not applied). */
+/* Single pair on DEVICE pointers (length only; budget not applied; 16-byte
+ * aligned buffers). */
 int wlcs_length_device(const uint8_t* d_x, size_t m, const uint8_t* d_y, size_t n, int variant,
                        uint32_t* out, void* stream);
 

@@ -36,7 +36,7 @@ constexpr int kMaxK = 8;
 constexpr int kNumClasses = 6 * kMaxK;   // S in {1,2,4,8,16,32} x K in 1..8
 constexpr int kChunkBuckets = 128;       // chunk-count buckets per class (clamped)
 constexpr int kBuckets = kNumClasses * kChunkBuckets;
-constexpr int kMapBytes = 256;
+constexpr int kMapBytes = 512;  // map [256] + inverse code list [256]
 constexpr uint32_t kNoBucket = 0xffffffffu;
 
 // meta[] layout (uint32)
@@ -71,7 +71,7 @@ __global__ void __launch_bounds__(256) batch_plan_kernel(BatchDev d, uint32_t* h
             d.out[p] = 0;  // empty input: length 0 (proj/tests/test_parallel.cpp:236-242)
         } else {
             const uint64_t w = (cols + 31) / 32;
-            if (w > uint64_t(32 * kMaxK)) {
+            if (w > uint64_t(32 * kMaxK) || rows > (uint64_t(1) << 30)) {
                 // Wider than one warp can hold: routed to the single-pair strip kernel.
                 const uint32_t i = atomicAdd(d.meta + kMetaOverflow, 1u);
                 d.overflow[i] = p;
@@ -187,15 +187,80 @@ __device__ __forceinline__ LanePair lane_pair(const BatchDev& d, bool active, ui
     return p;
 }
 
+// Decoded warp task t: pairs [first, last) of one lane shape (S, K).
+struct TaskInfo {
+    int sidx, S, K;
+    uint32_t first, last;
+};
+
+__device__ __forceinline__ TaskInfo decode_task(const BatchDev& d, uint32_t t, uint32_t lane) {
+    const uint32_t* count = d.meta + kMetaCount;
+    const uint32_t* pair_start = d.meta + kMetaPairStart;
+    const uint32_t* task_start = d.meta + kMetaTaskStart;
+    const bool le0 = task_start[lane] <= t;
+    const bool le1 = lane + 32 < kNumClasses && task_start[lane + 32] <= t;
+    const int order = __popc(__ballot_sync(kFullMask, le0)) +
+                      __popc(__ballot_sync(kFullMask, le1)) - 1;
+    const int c = kNumClasses - 1 - order;
+    TaskInfo ti;
+    ti.sidx = c / kMaxK;
+    ti.K = c % kMaxK + 1;
+    ti.S = 1 << ti.sidx;
+    const uint32_t per_task = 32u >> ti.sidx;
+    ti.first = pair_start[order] + (t - task_start[order]) * per_task;
+    const uint32_t end = pair_start[order] + count[order];
+    ti.last = ti.first + per_task < end ? ti.first + per_task : end;
+    return ti;
+}
+
+// ---------------------------------------------------------------------------
+// Match-mask build (per warp task, in the sweep kernel).
+//
+// Each lane owns K consecutive words (32*K columns) of its pair's column
+// string.  Per word the lane (1) realigns the 32 column bytes out of 16-byte
+// aligned chunks (funnel shifts), (2) turns them into 8 bit-planes with four
+// 8x8 bit transposes (plane b, bit j = bit b of column j's byte) and marks
+// the bytes present.  After the warp's prefix scan has assigned dense codes,
+// every code's match mask is the AND over the planes of "plane == bit of the
+// code's byte value": a handful of LOP3 per (code, word), written once --
+// no read-modify-write, no dependency chains, ALU only.
+__device__ __forceinline__ uint64_t transpose8x8(uint64_t x) {
+    uint64_t t = (x ^ (x >> 7)) & 0x00AA00AA00AA00AAull;
+    x = x ^ t ^ (t << 7);
+    t = (x ^ (x >> 14)) & 0x0000CCCC0000CCCCull;
+    x = x ^ t ^ (t << 14);
+    t = (x ^ (x >> 28)) & 0x00000000F0F0F0F0ull;
+    return x ^ t ^ (t << 28);
+}
+
+// 32 column bytes (8 words, byte j of the word = column j) -> 8 bit-planes.
+__device__ __forceinline__ void bit_planes(const uint32_t* w, uint32_t* P) {
+    uint32_t lo[4], hi[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const uint64_t y = transpose8x8(uint64_t(w[2 * q]) | (uint64_t(w[2 * q + 1]) << 32));
+        lo[q] = uint32_t(y);          // planes 0..3, 8 columns each
+        hi[q] = uint32_t(y >> 32);    // planes 4..7
+    }
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+        const uint32_t sel = 0x0040u | uint32_t(b) | (uint32_t(b) << 4);  // bytes b of x, y
+        P[b] = __byte_perm(__byte_perm(lo[0], lo[1], sel), __byte_perm(lo[2], lo[3], sel), 0x5410);
+        P[b + 4] =
+            __byte_perm(__byte_perm(hi[0], hi[1], sel), __byte_perm(hi[2], hi[3], sel), 0x5410);
+    }
+}
+
 // Builds the task's byte -> code map and match masks in shared memory.  K is
-// a runtime value here (one copy of this code for every lane shape).
-// Returns sigma (codes incl. the zero row) or 0 when the task's alphabet does
-// not fit the warp's shared-memory slice; *zrep receives a byte value absent
-// from the alphabet, replicated x4 (used to blank invalid rows).
+// a runtime value (one copy of this code for every lane shape).  Returns
+// sigma (codes incl. the zero row) or 0 when the alphabet does not fit the
+// warp's shared-memory slice; *zrep receives a byte value absent from the
+// alphabet, replicated x4 (used to blank invalid rows in the sweep).
 __device__ __forceinline__ uint32_t build_task(const BatchDev& d, const LanePair& p, int K, int s,
                                             uint8_t* smem, uint32_t* zrep) {
     const uint32_t lane = lane_id();
-    uint8_t* map = smem;
+    uint8_t* map = smem;         // byte -> code
+    uint8_t* inv = smem + 256;   // code -> byte
     uint8_t* pm = smem + kMapBytes;
     const bool wide = K > 4;
     const uint32_t cs = wide ? 1024u : 128u * uint32_t(K == 3 ? 4 : K);
@@ -203,25 +268,59 @@ __device__ __forceinline__ uint32_t build_task(const BatchDev& d, const LanePair
 
     __syncwarp();
     reinterpret_cast<uint2*>(map)[lane] = make_uint2(0u, 0u);
-    __syncwarp();
 
-    // The lane's columns: [c0, c0 + clen) of its pair's column string, read in
-    // 16-byte aligned chunks.
+    // The lane's columns [c0, c0 + clen): chunks 0..2K of the 16-byte aligned
+    // region starting a_c bytes before them, all loads issued up front.
     const int c0 = 32 * K * s;
     const int clen = max(min(c0 + 32 * K, p.cols) - c0, 0);
     const uint8_t* cbase = p.colp + c0;
     const int a_c = int(reinterpret_cast<uintptr_t>(cbase) & 15u);
     const uint8_t* cstart = cbase - a_c;
-    const int nch = clen > 0 ? (a_c + clen + 15) >> 4 : 0;
-    const int nch_max = warp_max(nch);
-    for (int ch = 0; ch < nch_max; ++ch) {
-        const uint32_t vm = ch < nch ? valid_mask16(ch * 16 - a_c, clen) : 0u;
-        const uint4 c = fetch_chunk(cstart, ch, vm, p.col_lo, p.col_hi, d.safe16);
+    uint4 chk[2 * kMaxK + 1];
 #pragma unroll
-        for (int r = 0; r < 16; ++r)
-            if ((vm >> r) & 1u) map[chunk_byte(c, r)] = 1;
+    for (int i = 0; i < 2 * kMaxK + 1; ++i) {
+        const uint32_t vm = i <= 2 * K ? valid_mask16(16 * i - a_c, clen) : 0u;
+        chk[i] = fetch_chunk(cstart, i, vm, p.col_lo, p.col_hi, d.safe16);
+    }
+    __syncwarp();  // map zeroed
+
+    // planes + presence marks, word by word
+    const int q = a_c >> 2;
+    const uint32_t fs = uint32_t(a_c & 3) * 8u;
+    uint32_t P[kMaxK][8];
+    uint32_t vmask[kMaxK];
+#pragma unroll
+    for (int k = 0; k < kMaxK; ++k) {
+        if (k < K) {
+            const uint32_t W[12] = {chk[2 * k].x,     chk[2 * k].y,     chk[2 * k].z,
+                                    chk[2 * k].w,     chk[2 * k + 1].x, chk[2 * k + 1].y,
+                                    chk[2 * k + 1].z, chk[2 * k + 1].w, chk[2 * k + 2].x,
+                                    chk[2 * k + 2].y, chk[2 * k + 2].z, chk[2 * k + 2].w};
+            uint32_t lo[9];
+#pragma unroll
+            for (int i = 0; i < 9; ++i) {
+                const uint32_t a = (q & 1) ? W[i + 1] : W[i];
+                const uint32_t b2 = (q & 1) ? W[i + 3] : W[i + 2];
+                lo[i] = (q & 2) ? b2 : a;
+            }
+            uint32_t w[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) w[i] = __funnelshift_r(lo[i], lo[i + 1], fs);
+            const int nv = min(max(clen - 32 * k, 0), 32);
+            vmask[k] = nv >= 32 ? 0xffffffffu : ((1u << nv) - 1u);
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+                if ((vmask[k] >> j) & 1u) map[__byte_perm(w[j >> 2], 0u, 0x4440u | uint32_t(j & 3))] = 1;
+            bit_planes(w, P[k]);
+        } else {
+            vmask[k] = 0u;
+#pragma unroll
+            for (int b = 0; b < 8; ++b) P[k][b] = 0u;
+        }
     }
     __syncwarp();
+
+    // dense codes 1..sigma-1 in byte order (0 = no match), inverse list, zrep
     uint32_t sigma;
     {
         const uint2 f = reinterpret_cast<const uint2*>(map)[lane];
@@ -237,48 +336,63 @@ __device__ __forceinline__ uint32_t build_task(const BatchDev& d, const LanePair
             const uint32_t v = __shfl_up_sync(kFullMask, incl, o);
             if (int(lane) >= o) incl += v;
         }
+        sigma = __shfl_sync(kFullMask, incl, 31) + 1;  // + the zero row
+        if (sigma > 256u || sigma * cs > uint32_t(d.pm_bytes)) return 0u;
         uint32_t code = incl - cnt + 1;
         uint32_t ox = 0, oy = 0;
 #pragma unroll
-        for (int b = 0; b < 4; ++b)
-            if ((present >> b) & 1u) ox |= (code++) << (8 * b);
-#pragma unroll
-        for (int b = 0; b < 4; ++b)
-            if ((present >> (b + 4)) & 1u) oy |= (code++) << (8 * b);
-        sigma = __shfl_sync(kFullMask, incl, 31) + 1;  // + the zero row
-        if (sigma > 256u || sigma * cs > uint32_t(d.pm_bytes)) return 0u;
-        // an absent byte value (exists: at most 255 are present)
-        const uint32_t absent = ~present & 0xffu;
+        for (int b = 0; b < 8; ++b) {
+            if ((present >> b) & 1u) {
+                if (b < 4) ox |= code << (8 * b);
+                else oy |= code << (8 * (b - 4));
+                inv[code] = uint8_t(8 * lane + uint32_t(b));
+                ++code;
+            }
+        }
+        const uint32_t absent = ~present & 0xffu;  // exists: at most 255 bytes present
         const uint32_t has = __ballot_sync(kFullMask, absent != 0u);
-        const int zl = __ffs(has) - 1;
-        const uint32_t zb = __shfl_sync(kFullMask, uint32_t(8 * lane) + __ffs(absent) - 1, zl);
+        const uint32_t zb =
+            __shfl_sync(kFullMask, uint32_t(8 * lane) + __ffs(absent) - 1, __ffs(has) - 1);
         *zrep = zb * 0x01010101u;
+        __syncwarp();
         reinterpret_cast<uint2*>(map)[lane] = make_uint2(ox, oy);
-        uint4* pm4 = reinterpret_cast<uint4*>(pm);
-        for (uint32_t i = lane; i < sigma * (cs / 16); i += 32) pm4[i] = make_uint4(0, 0, 0, 0);
     }
     __syncwarp();
 
-    // Match masks: bit (j - c0) of the lane's K words for every column j.  A
-    // 16-column chunk touches at most two words: A (its first column's) and B.
-    for (int ch = 0; ch < nch_max; ++ch) {
-        const int jr0 = ch * 16 - a_c;
-        const uint32_t vm = ch < nch ? valid_mask16(jr0, clen) : 0u;
-        const uint4 c = fetch_chunk(cstart, ch, vm, p.col_lo, p.col_hi, d.safe16);
-        const int sh0 = jr0 & 31;
-        const int w0 = jr0 >> 5;
-        const int w1 = w0 + 1;
-        const uint32_t woffA = wide ? uint32_t((w0 >> 2) * 512 + (w0 & 3) * 4) + lane * 16u
-                                    : lane * ls + uint32_t(w0 * 4);
-        const uint32_t woffB = wide ? uint32_t((w1 >> 2) * 512 + (w1 & 3) * 4) + lane * 16u
-                                    : lane * ls + uint32_t(w1 * 4);
+    // code 0: the zero row
+    const uint32_t lane_off = wide ? lane * 16u : lane * ls;
 #pragma unroll
-        for (int r = 0; r < 16; ++r) {
-            if ((vm >> r) & 1u) {
-                const int t = sh0 + r;
-                const uint32_t code = map[chunk_byte(c, r)];
-                uint32_t* wp = reinterpret_cast<uint32_t*>(pm + code * cs + (t < 32 ? woffA : woffB));
-                *wp |= 1u << (t & 31);
+    for (int k = 0; k < kMaxK; ++k) {
+        if (k < K) {
+            const uint32_t woff = wide ? uint32_t((k >> 2) * 512 + (k & 3) * 4) : uint32_t(k * 4);
+            *reinterpret_cast<uint32_t*>(pm + lane_off + woff) = 0u;
+        }
+    }
+    // codes 1..sigma-1: mask = valid columns whose byte equals the code's byte
+    uint32_t hi_acc[kMaxK];
+    uint32_t hi_v = 0xffffffffu;
+    for (uint32_t c = 1; c < sigma; ++c) {
+        const uint32_t v = inv[c];
+        if ((v >> 4) != hi_v) {  // warp-uniform: codes are sorted by byte value
+            hi_v = v >> 4;
+            const uint32_t U4 = 0u - ((v >> 4) & 1u), U5 = 0u - ((v >> 5) & 1u);
+            const uint32_t U6 = 0u - ((v >> 6) & 1u), U7 = 0u - ((v >> 7) & 1u);
+#pragma unroll
+            for (int k = 0; k < kMaxK; ++k)
+                hi_acc[k] = ~((P[k][4] ^ U4) | (P[k][5] ^ U5) | (P[k][6] ^ U6) | (P[k][7] ^ U7)) &
+                            vmask[k];
+        }
+        const uint32_t U0 = 0u - (v & 1u), U1 = 0u - ((v >> 1) & 1u);
+        const uint32_t U2 = 0u - ((v >> 2) & 1u), U3 = 0u - ((v >> 3) & 1u);
+        uint8_t* row = pm + c * cs + lane_off;
+#pragma unroll
+        for (int k = 0; k < kMaxK; ++k) {
+            if (k < K) {
+                const uint32_t m = hi_acc[k] & ~((P[k][0] ^ U0) | (P[k][1] ^ U1) |
+                                                 (P[k][2] ^ U2) | (P[k][3] ^ U3));
+                const uint32_t woff =
+                    wide ? uint32_t((k >> 2) * 512 + (k & 3) * 4) : uint32_t(k * 4);
+                *reinterpret_cast<uint32_t*>(row + woff) = m;
             }
         }
     }
@@ -333,34 +447,20 @@ __device__ __forceinline__ int sweep_task(const BatchDev& d, const LanePair& p, 
         break;
 
 __global__ void __launch_bounds__(32) batch_main_kernel(BatchDev d) {
-    extern __shared__ __align__(16) uint8_t smem[];
+    extern __shared__ __align__(16) uint8_t smem[];  // map [256] | inv [256] | PM
     const uint32_t lane = lane_id();
-    const uint32_t* count = d.meta + kMetaCount;
-    const uint32_t* pair_start = d.meta + kMetaPairStart;
-    const uint32_t* task_start = d.meta + kMetaTaskStart;
-    const uint32_t total = task_start[kNumClasses];
+    const uint32_t total = d.meta[kMetaTaskStart + kNumClasses];
     for (;;) {
         uint32_t t = 0;
         if (lane == 0) t = atomicAdd(d.meta + kMetaCounter, 1u);
         t = __shfl_sync(kFullMask, t, 0);
         if (t >= total) break;
-        const bool le0 = task_start[lane] <= t;
-        const bool le1 = lane + 32 < kNumClasses && task_start[lane + 32] <= t;
-        const int order = __popc(__ballot_sync(kFullMask, le0)) +
-                          __popc(__ballot_sync(kFullMask, le1)) - 1;
-        const int c = kNumClasses - 1 - order;
-        const int sidx = c / kMaxK;
-        const int K = c % kMaxK + 1;
-        const int S = 1 << sidx;
-        const uint32_t per_task = 32u >> sidx;
-        const uint32_t first = pair_start[order] + (t - task_start[order]) * per_task;
-        const uint32_t end = pair_start[order] + count[order];
-        const uint32_t last = first + per_task < end ? first + per_task : end;
-
-        const int seg = int(lane) >> sidx;
+        const TaskInfo ti = decode_task(d, t, lane);
+        const int K = ti.K;
+        const int S = ti.S;
         const int s = int(lane) & (S - 1);
-        const uint32_t idx = first + uint32_t(seg);
-        const bool active = idx < last;
+        const uint32_t idx = ti.first + (lane >> ti.sidx);
+        const bool active = idx < ti.last;
         const uint32_t pair = active ? d.vals[idx] : 0u;
         const LanePair p = lane_pair(d, active, pair);
         uint32_t zrep = 0;
@@ -387,8 +487,7 @@ __global__ void __launch_bounds__(32) batch_main_kernel(BatchDev d) {
 
 }  // namespace
 
-size_t batch_workspace_bytes(uint32_t pairs, size_t* aux_bytes) {
-    *aux_bytes = 0;
+size_t batch_workspace_bytes(uint32_t pairs, int /*pm_bytes*/) {
     return (kWsPairs + 3 * size_t(pairs)) * sizeof(uint32_t);
 }
 
@@ -397,8 +496,8 @@ int batch_smem_per_cta(int pm_bytes) { return kMapBytes + pm_bytes; }
 // Enqueue the whole batch on `stream` (device pointers only).  Pairs routed to
 // the single-pair path are listed in the workspace (batch_overflow_*_ptr).
 // Optional events bracket the main kernel (bench.py's roofline timing).
-cudaError_t batch_launch(BatchDev d, void* workspace, size_t /*aux_bytes*/, int sms,
-                         cudaStream_t stream, cudaEvent_t ev_main0, cudaEvent_t ev_main1) {
+cudaError_t batch_launch(BatchDev d, void* workspace, int sms, cudaStream_t stream,
+                         cudaEvent_t ev_main0, cudaEvent_t ev_main1) {
     uint32_t* ws = static_cast<uint32_t*>(workspace);
     d.meta = ws;
     d.safe16 = reinterpret_cast<const uint4*>(ws + kMetaSafe16);
@@ -414,10 +513,13 @@ cudaError_t batch_launch(BatchDev d, void* workspace, size_t /*aux_bytes*/, int 
     batch_plan_kernel<<<blocks, 256, 0, stream>>>(d, hist, bucket);
     batch_scan_kernel<<<1, 1024, 0, stream>>>(d, hist, cursor);
     batch_scatter_kernel<<<blocks, 256, 0, stream>>>(d, bucket, cursor);
+    int occ = 0;
     const int smem = batch_smem_per_cta(d.pm_bytes);
     e = cudaFuncSetAttribute(batch_main_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    int occ = 0;
+    e = cudaFuncSetAttribute(batch_main_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             cudaSharedmemCarveoutMaxShared);
+    if (e != cudaSuccess) return e;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, batch_main_kernel, 32, smem);
     if (e != cudaSuccess) return e;
     if (occ < 1) occ = 1;
@@ -427,11 +529,11 @@ cudaError_t batch_launch(BatchDev d, void* workspace, size_t /*aux_bytes*/, int 
     return cudaGetLastError();
 }
 
-uint32_t* batch_overflow_count_ptr(void* workspace, size_t, uint32_t) {
+uint32_t* batch_overflow_count_ptr(void* workspace, uint32_t) {
     return static_cast<uint32_t*>(workspace) + kMetaOverflow;
 }
 
-uint32_t* batch_overflow_list_ptr(void* workspace, size_t, uint32_t pairs) {
+uint32_t* batch_overflow_list_ptr(void* workspace, uint32_t pairs) {
     return static_cast<uint32_t*>(workspace) + kWsPairs + 2 * size_t(pairs);
 }
 

@@ -251,8 +251,8 @@ int batch_device(Ctx& c, const uint8_t* d_xs, const uint64_t* d_xoff, const uint
     if (variant != WLCS_VARIANT_BITPARALLEL)
         return fail(WLCS_E_CONFIG, "fill variant " + std::to_string(variant) +
                                        " is not available for batches");
-    size_t cub_bytes = 0;
-    const size_t ws_bytes = wlcs::batch_workspace_bytes(uint32_t(pairs), &cub_bytes);
+    const int pm_bytes = env_int("WLCS_BATCH_PM_KB", 24) * 1024;
+    const size_t ws_bytes = wlcs::batch_workspace_bytes(uint32_t(pairs), pm_bytes);
     WLCS_CUDA(c.ws.ensure(ws_bytes));
     wlcs::BatchDev d{};
     d.xs = d_xs;
@@ -263,23 +263,23 @@ int batch_device(Ctx& c, const uint8_t* d_xs, const uint64_t* d_xoff, const uint
     d.ys_bytes = ys_bytes;
     d.out = d_out;
     d.pairs = uint32_t(pairs);
-    d.pm_bytes = env_int("WLCS_BATCH_PM_KB", 24) * 1024;
+    d.pm_bytes = pm_bytes;
     if (c.timing && !c.ev0) {
         WLCS_CUDA(cudaEventCreate(&c.ev0));
         WLCS_CUDA(cudaEventCreate(&c.ev1));
     }
-    WLCS_CUDA(wlcs::batch_launch(d, c.ws.p, cub_bytes, c.sms, stream, c.timing ? c.ev0 : nullptr,
+    WLCS_CUDA(wlcs::batch_launch(d, c.ws.p, c.sms, stream, c.timing ? c.ev0 : nullptr,
                                  c.timing ? c.ev1 : nullptr));
     uint32_t overflow = 0;
     WLCS_CUDA(cudaMemcpyAsync(&overflow,
-                              wlcs::batch_overflow_count_ptr(c.ws.p, cub_bytes, uint32_t(pairs)),
+                              wlcs::batch_overflow_count_ptr(c.ws.p, uint32_t(pairs)),
                               4, cudaMemcpyDeviceToHost, stream));
     WLCS_CUDA(cudaStreamSynchronize(stream));
     if (c.timing) WLCS_CUDA(cudaEventElapsedTime(&c.last_main_ms, c.ev0, c.ev1));
     if (overflow == 0) return WLCS_OK;
     // Pairs too long or with too large an alphabet for one warp: strip kernel.
     std::vector<uint32_t> ids(overflow);
-    WLCS_CUDA(cudaMemcpy(ids.data(), wlcs::batch_overflow_list_ptr(c.ws.p, cub_bytes, uint32_t(pairs)),
+    WLCS_CUDA(cudaMemcpy(ids.data(), wlcs::batch_overflow_list_ptr(c.ws.p, uint32_t(pairs)),
                          overflow * 4, cudaMemcpyDeviceToHost));
     for (uint32_t p : ids) {
         uint64_t xo[2], yo[2];
@@ -358,6 +358,8 @@ int wlcs_length_device(const uint8_t* d_x, size_t m, const uint8_t* d_y, size_t 
                        uint32_t* out, void* stream) {
     (void)stream;
     if (!out) return fail(WLCS_E_INVALID_ARGUMENT, "out is NULL");
+    if ((reinterpret_cast<uintptr_t>(d_x) | reinterpret_cast<uintptr_t>(d_y)) & 15u)
+        return fail(WLCS_E_INVALID_ARGUMENT, "device string buffers must be 16-byte aligned");
     Ctx* c = nullptr;
     int rc = get_ctx(&c);
     if (rc) return rc;
@@ -413,6 +415,8 @@ int wlcs_subsequence(const uint8_t* x, size_t m, const uint8_t* y, size_t n,
 int wlcs_length_batch_device(const uint8_t* d_xs, const uint64_t* d_x_off, const uint8_t* d_ys,
                              const uint64_t* d_y_off, size_t pairs, uint64_t xs_bytes,
                              uint64_t ys_bytes, int variant, uint32_t* d_out, void* stream) {
+    if ((reinterpret_cast<uintptr_t>(d_xs) | reinterpret_cast<uintptr_t>(d_ys)) & 15u)
+        return fail(WLCS_E_INVALID_ARGUMENT, "device string buffers must be 16-byte aligned");
     Ctx* c = nullptr;
     int rc = get_ctx(&c);
     if (rc) return rc;

@@ -29,14 +29,13 @@ struct BatchDev {
     const uint4* safe16;   // 16 zero bytes in device memory
 };
 
-size_t batch_workspace_bytes(uint32_t pairs, size_t* cub_bytes);
+size_t batch_workspace_bytes(uint32_t pairs, int pm_bytes);
 int batch_smem_per_cta(int pm_bytes);
-cudaError_t batch_launch(BatchDev d, void* workspace, size_t cub_bytes, int sms,
-                         cudaStream_t stream, cudaEvent_t ev_main0 = nullptr,
-                         cudaEvent_t ev_main1 = nullptr);
+cudaError_t batch_launch(BatchDev d, void* workspace, int sms, cudaStream_t stream,
+                         cudaEvent_t ev_main0 = nullptr, cudaEvent_t ev_main1 = nullptr);
 cudaError_t int_peak_probe(int reps, double* ops_per_s, uint32_t* scratch);
-uint32_t* batch_overflow_count_ptr(void* workspace, size_t cub_bytes, uint32_t pairs);
-uint32_t* batch_overflow_list_ptr(void* workspace, size_t cub_bytes, uint32_t pairs);
+uint32_t* batch_overflow_count_ptr(void* workspace, uint32_t pairs);
+uint32_t* batch_overflow_list_ptr(void* workspace, uint32_t pairs);
 
 }  // namespace wlcs
 
