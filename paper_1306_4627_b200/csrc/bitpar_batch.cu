@@ -48,25 +48,29 @@ constexpr int kMetaOverflow = 3 * kNumClasses + 2;
 constexpr int kMetaSafe16 = 240;                          // 16 zero bytes (fetch_chunk)
 constexpr int kMetaWords = 256;
 // workspace (uint32): meta[256] | hist[kBuckets] | cursor[kBuckets] |
-//                     bucket[pairs] | vals[pairs] | overflow[pairs]
+//                     bucket[pairs] | vals[pairs] | overflow[pairs] | rank[pairs]
 constexpr size_t kWsHist = kMetaWords;
 constexpr size_t kWsCursor = kWsHist + kBuckets;
 constexpr size_t kWsPairs = kWsCursor + kBuckets;
 
 __device__ __forceinline__ int class_of(int sidx, int k) { return sidx * kMaxK + (k - 1); }
 
+// One thread per pair.  Besides the bucket it records the pair's rank inside
+// its bucket: a block-local rank (shared-memory atomics) plus the block's base
+// in that bucket (one global atomic per block and bucket), so the scatter
+// needs no atomics.
 __global__ void __launch_bounds__(256) batch_plan_kernel(BatchDev d, uint32_t* hist,
-                                                         uint32_t* bucket) {
+                                                         uint32_t* bucket, uint32_t* rank) {
     __shared__ uint32_t local[kBuckets];
     for (int i = threadIdx.x; i < kBuckets; i += blockDim.x) local[i] = 0;
     __syncthreads();
     const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+    uint32_t b = kNoBucket, r = 0;
     if (p < d.pairs) {
         const uint64_t m = d.xoff[p + 1] - d.xoff[p];
         const uint64_t n = d.yoff[p + 1] - d.yoff[p];
         const uint64_t cols = m < n ? m : n;
         const uint64_t rows = m < n ? n : m;
-        uint32_t b = kNoBucket;
         if (cols == 0) {
             d.out[p] = 0;  // empty input: length 0 (proj/tests/test_parallel.cpp:236-242)
         } else {
@@ -84,14 +88,20 @@ __global__ void __launch_bounds__(256) batch_plan_kernel(BatchDev d, uint32_t* h
                 uint64_t nch = (rows + 15) / 16;
                 if (nch > kChunkBuckets - 1) nch = kChunkBuckets - 1;
                 b = uint32_t(order * kChunkBuckets + (kChunkBuckets - 1 - int(nch)));
-                atomicAdd(&local[b], 1u);
+                r = atomicAdd(&local[b], 1u);
             }
         }
-        bucket[p] = b;
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < kBuckets; i += blockDim.x)
-        if (local[i]) atomicAdd(hist + i, local[i]);
+    for (int i = threadIdx.x; i < kBuckets; i += blockDim.x) {
+        const uint32_t c = local[i];
+        if (c) local[i] = atomicAdd(hist + i, c);  // block base inside bucket i
+    }
+    __syncthreads();
+    if (p < d.pairs) {
+        bucket[p] = b;
+        rank[p] = b == kNoBucket ? 0u : local[b] + r;
+    }
 }
 
 // One CTA: exclusive scan of the bucket histogram -> cursors, per-class pair
@@ -153,12 +163,13 @@ __global__ void __launch_bounds__(1024) batch_scan_kernel(BatchDev d, const uint
 }
 
 __global__ void __launch_bounds__(256) batch_scatter_kernel(BatchDev d, const uint32_t* bucket,
-                                                            uint32_t* cursor) {
+                                                            const uint32_t* rank,
+                                                            const uint32_t* start) {
     const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= d.pairs) return;
     const uint32_t b = bucket[p];
     if (b == kNoBucket) return;
-    d.vals[atomicAdd(cursor + b, 1u)] = p;
+    d.vals[start[b] + rank[p]] = p;
 }
 
 // Per-lane view of its pair inside a task.
@@ -266,8 +277,14 @@ __device__ __forceinline__ uint32_t build_task(const BatchDev& d, const LanePair
     const uint32_t cs = wide ? 1024u : 128u * uint32_t(K == 3 ? 4 : K);
     const uint32_t ls = wide ? 16u : 4u * uint32_t(K == 3 ? 4 : K);
 
+    // presence flags: one 32-bit word per byte value in the (not yet used) PM
+    // region -- lanes marking the same byte hit the same word (no conflict),
+    // different bytes hit different banks
+    uint32_t* flags = reinterpret_cast<uint32_t*>(pm);
     __syncwarp();
-    reinterpret_cast<uint2*>(map)[lane] = make_uint2(0u, 0u);
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+        reinterpret_cast<uint4*>(flags)[lane * 2 + i] = make_uint4(0u, 0u, 0u, 0u);
 
     // The lane's columns [c0, c0 + clen): chunks 0..2K of the 16-byte aligned
     // region starting a_c bytes before them, all loads issued up front.
@@ -282,7 +299,7 @@ __device__ __forceinline__ uint32_t build_task(const BatchDev& d, const LanePair
         const uint32_t vm = i <= 2 * K ? valid_mask16(16 * i - a_c, clen) : 0u;
         chk[i] = fetch_chunk(cstart, i, vm, p.col_lo, p.col_hi, d.safe16);
     }
-    __syncwarp();  // map zeroed
+    __syncwarp();  // flags zeroed
 
     // planes + presence marks, word by word
     const int q = a_c >> 2;
@@ -310,7 +327,7 @@ __device__ __forceinline__ uint32_t build_task(const BatchDev& d, const LanePair
             vmask[k] = nv >= 32 ? 0xffffffffu : ((1u << nv) - 1u);
 #pragma unroll
             for (int j = 0; j < 32; ++j)
-                if ((vmask[k] >> j) & 1u) map[__byte_perm(w[j >> 2], 0u, 0x4440u | uint32_t(j & 3))] = 1;
+                if ((vmask[k] >> j) & 1u) flags[__byte_perm(w[j >> 2], 0u, 0x4440u | uint32_t(j & 3))] = 1u;
             bit_planes(w, P[k]);
         } else {
             vmask[k] = 0u;
@@ -323,12 +340,11 @@ __device__ __forceinline__ uint32_t build_task(const BatchDev& d, const LanePair
     // dense codes 1..sigma-1 in byte order (0 = no match), inverse list, zrep
     uint32_t sigma;
     {
-        const uint2 f = reinterpret_cast<const uint2*>(map)[lane];
-        uint32_t present = 0;  // bit b: byte 8*lane + b present
-#pragma unroll
-        for (int b = 0; b < 4; ++b) present |= (((f.x >> (8 * b)) & 0xffu) ? 1u : 0u) << b;
-#pragma unroll
-        for (int b = 0; b < 4; ++b) present |= (((f.y >> (8 * b)) & 0xffu) ? 1u : 0u) << (b + 4);
+        const uint4 f0 = reinterpret_cast<const uint4*>(flags)[lane * 2];
+        const uint4 f1 = reinterpret_cast<const uint4*>(flags)[lane * 2 + 1];
+        const uint32_t present = (f0.x ? 1u : 0u) | (f0.y ? 2u : 0u) | (f0.z ? 4u : 0u) |
+                                 (f0.w ? 8u : 0u) | (f1.x ? 16u : 0u) | (f1.y ? 32u : 0u) |
+                                 (f1.z ? 64u : 0u) | (f1.w ? 128u : 0u);  // byte 8*lane + b
         const uint32_t cnt = __popc(present);
         uint32_t incl = cnt;
 #pragma unroll
@@ -432,9 +448,12 @@ __device__ __forceinline__ int sweep_task(const BatchDev& d, const LanePair& p, 
             cout = 0;
         }
         if (!__all_sync(kFullMask, vm == 0xffffu)) cur = sanitize_chunk(cur, vm, zrep);
-        uint32_t off[16];
-        chunk_offsets(cur, map, cs, lane_off, off);
-        rows16<CHAIN, K>(V, pm, off, vm, cin, cout, NoRowHook{});
+#pragma unroll 1
+        for (int h = 0; h < 2; ++h) {
+            const uint32_t lo = h ? cur.z : cur.x;
+            const uint32_t hi = h ? cur.w : cur.y;
+            rows8<CHAIN, K>(V, map, pm, cs, lane_off, lo, hi, cin, cout);
+        }
         cur = nxt;
         vm = vm_next;
     }
@@ -488,7 +507,7 @@ __global__ void __launch_bounds__(32) batch_main_kernel(BatchDev d) {
 }  // namespace
 
 size_t batch_workspace_bytes(uint32_t pairs, int /*pm_bytes*/) {
-    return (kWsPairs + 3 * size_t(pairs)) * sizeof(uint32_t);
+    return (kWsPairs + 4 * size_t(pairs)) * sizeof(uint32_t);
 }
 
 int batch_smem_per_cta(int pm_bytes) { return kMapBytes + pm_bytes; }
@@ -506,13 +525,14 @@ cudaError_t batch_launch(BatchDev d, void* workspace, int sms, cudaStream_t stre
     uint32_t* bucket = ws + kWsPairs;
     d.vals = bucket + d.pairs;
     d.overflow = d.vals + d.pairs;
+    uint32_t* rank = d.overflow + d.pairs;
     cudaError_t e = cudaMemsetAsync(ws, 0, kWsCursor * sizeof(uint32_t), stream);  // meta + hist
     if (e != cudaSuccess) return e;
     if (d.pairs == 0) return cudaSuccess;
     const int blocks = int((d.pairs + 255) / 256);
-    batch_plan_kernel<<<blocks, 256, 0, stream>>>(d, hist, bucket);
+    batch_plan_kernel<<<blocks, 256, 0, stream>>>(d, hist, bucket, rank);
     batch_scan_kernel<<<1, 1024, 0, stream>>>(d, hist, cursor);
-    batch_scatter_kernel<<<blocks, 256, 0, stream>>>(d, bucket, cursor);
+    batch_scatter_kernel<<<blocks, 256, 0, stream>>>(d, bucket, rank, cursor);
     int occ = 0;
     const int smem = batch_smem_per_cta(d.pm_bytes);
     e = cudaFuncSetAttribute(batch_main_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);

@@ -122,6 +122,22 @@ __device__ __forceinline__ void rows16(uint32_t* V, const uint8_t* pm, const uin
     }
 }
 
+// Half-chunk variant used by the batch sweep: rows 8h..8h+7 of the chunk
+// (bytes in lo = word 2h, hi = word 2h+1), emitted once inside a rolled loop
+// over the two halves so each sweep instance stays small in the I-cache.
+template <bool CHAIN, int K, typename MapT>
+__device__ __forceinline__ void rows8(uint32_t* V, const MapT* map, const uint8_t* pm,
+                                      uint32_t cs, uint32_t lane_off, uint32_t lo, uint32_t hi,
+                                      uint32_t& cin, uint32_t& cout) {
+    uint32_t off[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+        off[r] = uint32_t(map[__byte_perm(r < 4 ? lo : hi, 0u, 0x4440u | uint32_t(r & 3))]) * cs +
+                 lane_off;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) row_update<CHAIN, K>(V, pm, off[r], cin, cout);
+}
+
 // The 16-byte chunk `ch` of a lane's row string (chunk addresses are 16-byte
 // aligned by construction).  The common case is one unconditional LDG.128 the
 // compiler can hoist a whole step ahead of its use; straddling chunks take a
