@@ -262,10 +262,28 @@ __device__ __forceinline__ void bit_planes(const uint32_t* w, uint32_t* P) {
     }
 }
 
+// The 32 column bytes of the lane's word k, realigned out of the 16-byte
+// aligned chunks 2k, 2k+1, 2k+2 (q = a_c / 4, fs = 8 * (a_c % 4)).
+__device__ __forceinline__ void word_bytes(const uint4& c0, const uint4& c1, const uint4& c2, int q,
+                                           uint32_t fs, uint32_t* w) {
+    const uint32_t W[12] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w, c2.x, c2.y, c2.z, c2.w};
+    uint32_t lo[9];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) {
+        const uint32_t a = (q & 1) ? W[i + 1] : W[i];
+        const uint32_t b2 = (q & 1) ? W[i + 3] : W[i + 2];
+        lo[i] = (q & 2) ? b2 : a;
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) w[i] = __funnelshift_r(lo[i], lo[i + 1], fs);
+}
+
 // Builds the task's byte -> code map and match masks in shared memory.  K is
-// a runtime value (one copy of this code for every lane shape).  Returns
-// sigma (codes incl. the zero row) or 0 when the alphabet does not fit the
-// warp's shared-memory slice; *zrep receives a byte value absent from the
+// a runtime value and every loop over words / codes is rolled: the build is
+// one small piece of code shared by all lane shapes (it runs once per task
+// while the sweep code is hot, so its I-cache footprint matters).
+// Returns sigma (codes incl. the zero row) or 0 when the alphabet does not fit
+// the warp's shared-memory slice; *zrep receives a byte value absent from the
 // alphabet, replicated x4 (used to blank invalid rows in the sweep).
 __device__ __forceinline__ uint32_t build_task(const BatchDev& d, const LanePair& p, int K, int s,
                                             uint8_t* smem, uint32_t* zrep) {
@@ -278,61 +296,43 @@ __device__ __forceinline__ uint32_t build_task(const BatchDev& d, const LanePair
     const uint32_t ls = wide ? 16u : 4u * uint32_t(K == 3 ? 4 : K);
 
     // presence flags: one 32-bit word per byte value in the (not yet used) PM
-    // region -- lanes marking the same byte hit the same word (no conflict),
-    // different bytes hit different banks
+    // region -- lanes marking the same byte hit the same word (no conflict)
     uint32_t* flags = reinterpret_cast<uint32_t*>(pm);
     __syncwarp();
 #pragma unroll
     for (int i = 0; i < 2; ++i)
         reinterpret_cast<uint4*>(flags)[lane * 2 + i] = make_uint4(0u, 0u, 0u, 0u);
 
-    // The lane's columns [c0, c0 + clen): chunks 0..2K of the 16-byte aligned
-    // region starting a_c bytes before them, all loads issued up front.
+    // The lane's columns [c0, c0 + clen), read as the 16-byte aligned chunks
+    // 0..2K of the region starting a_c bytes before them.
     const int c0 = 32 * K * s;
     const int clen = max(min(c0 + 32 * K, p.cols) - c0, 0);
     const uint8_t* cbase = p.colp + c0;
     const int a_c = int(reinterpret_cast<uintptr_t>(cbase) & 15u);
     const uint8_t* cstart = cbase - a_c;
-    uint4 chk[2 * kMaxK + 1];
-#pragma unroll
-    for (int i = 0; i < 2 * kMaxK + 1; ++i) {
-        const uint32_t vm = i <= 2 * K ? valid_mask16(16 * i - a_c, clen) : 0u;
-        chk[i] = fetch_chunk(cstart, i, vm, p.col_lo, p.col_hi, d.safe16);
-    }
-    __syncwarp();  // flags zeroed
-
-    // planes + presence marks, word by word
     const int q = a_c >> 2;
     const uint32_t fs = uint32_t(a_c & 3) * 8u;
-    uint32_t P[kMaxK][8];
-    uint32_t vmask[kMaxK];
-#pragma unroll
-    for (int k = 0; k < kMaxK; ++k) {
-        if (k < K) {
-            const uint32_t W[12] = {chk[2 * k].x,     chk[2 * k].y,     chk[2 * k].z,
-                                    chk[2 * k].w,     chk[2 * k + 1].x, chk[2 * k + 1].y,
-                                    chk[2 * k + 1].z, chk[2 * k + 1].w, chk[2 * k + 2].x,
-                                    chk[2 * k + 2].y, chk[2 * k + 2].z, chk[2 * k + 2].w};
-            uint32_t lo[9];
-#pragma unroll
-            for (int i = 0; i < 9; ++i) {
-                const uint32_t a = (q & 1) ? W[i + 1] : W[i];
-                const uint32_t b2 = (q & 1) ? W[i + 3] : W[i + 2];
-                lo[i] = (q & 2) ? b2 : a;
-            }
+    auto chunk = [&](int i) {
+        const uint32_t vm = i <= 2 * K ? valid_mask16(16 * i - a_c, clen) : 0u;
+        return fetch_chunk(cstart, i, vm, p.col_lo, p.col_hi, d.safe16);
+    };
+    __syncwarp();  // flags zeroed
+
+    // pass 1: mark the bytes present (next word's chunks prefetched)
+    {
+        uint4 c0v = chunk(0), c1v = chunk(1), c2v = chunk(2);
+#pragma unroll 1
+        for (int k = 0; k < K; ++k) {
+            const uint4 n1 = chunk(2 * k + 3), n2 = chunk(2 * k + 4);
             uint32_t w[8];
-#pragma unroll
-            for (int i = 0; i < 8; ++i) w[i] = __funnelshift_r(lo[i], lo[i + 1], fs);
+            word_bytes(c0v, c1v, c2v, q, fs, w);
             const int nv = min(max(clen - 32 * k, 0), 32);
-            vmask[k] = nv >= 32 ? 0xffffffffu : ((1u << nv) - 1u);
 #pragma unroll
             for (int j = 0; j < 32; ++j)
-                if ((vmask[k] >> j) & 1u) flags[__byte_perm(w[j >> 2], 0u, 0x4440u | uint32_t(j & 3))] = 1u;
-            bit_planes(w, P[k]);
-        } else {
-            vmask[k] = 0u;
-#pragma unroll
-            for (int b = 0; b < 8; ++b) P[k][b] = 0u;
+                if (j < nv) flags[__byte_perm(w[j >> 2], 0u, 0x4440u | uint32_t(j & 3))] = 1u;
+            c0v = c2v;
+            c1v = n1;
+            c2v = n2;
         }
     }
     __syncwarp();
@@ -375,41 +375,40 @@ __device__ __forceinline__ uint32_t build_task(const BatchDev& d, const LanePair
     }
     __syncwarp();
 
-    // code 0: the zero row
+    // pass 2, word by word: bit-planes, then every code's match mask
+    // = valid columns whose byte equals the code's byte value.
     const uint32_t lane_off = wide ? lane * 16u : lane * ls;
-#pragma unroll
-    for (int k = 0; k < kMaxK; ++k) {
-        if (k < K) {
-            const uint32_t woff = wide ? uint32_t((k >> 2) * 512 + (k & 3) * 4) : uint32_t(k * 4);
-            *reinterpret_cast<uint32_t*>(pm + lane_off + woff) = 0u;
-        }
-    }
-    // codes 1..sigma-1: mask = valid columns whose byte equals the code's byte
-    uint32_t hi_acc[kMaxK];
-    uint32_t hi_v = 0xffffffffu;
-    for (uint32_t c = 1; c < sigma; ++c) {
-        const uint32_t v = inv[c];
-        if ((v >> 4) != hi_v) {  // warp-uniform: codes are sorted by byte value
-            hi_v = v >> 4;
-            const uint32_t U4 = 0u - ((v >> 4) & 1u), U5 = 0u - ((v >> 5) & 1u);
-            const uint32_t U6 = 0u - ((v >> 6) & 1u), U7 = 0u - ((v >> 7) & 1u);
-#pragma unroll
-            for (int k = 0; k < kMaxK; ++k)
-                hi_acc[k] = ~((P[k][4] ^ U4) | (P[k][5] ^ U5) | (P[k][6] ^ U6) | (P[k][7] ^ U7)) &
-                            vmask[k];
-        }
-        const uint32_t U0 = 0u - (v & 1u), U1 = 0u - ((v >> 1) & 1u);
-        const uint32_t U2 = 0u - ((v >> 2) & 1u), U3 = 0u - ((v >> 3) & 1u);
-        uint8_t* row = pm + c * cs + lane_off;
-#pragma unroll
-        for (int k = 0; k < kMaxK; ++k) {
-            if (k < K) {
-                const uint32_t m = hi_acc[k] & ~((P[k][0] ^ U0) | (P[k][1] ^ U1) |
-                                                 (P[k][2] ^ U2) | (P[k][3] ^ U3));
-                const uint32_t woff =
-                    wide ? uint32_t((k >> 2) * 512 + (k & 3) * 4) : uint32_t(k * 4);
-                *reinterpret_cast<uint32_t*>(row + woff) = m;
+    {
+        uint4 c0v = chunk(0), c1v = chunk(1), c2v = chunk(2);
+#pragma unroll 1
+        for (int k = 0; k < K; ++k) {
+            const uint4 n1 = chunk(2 * k + 3), n2 = chunk(2 * k + 4);
+            uint32_t w[8], P[8];
+            word_bytes(c0v, c1v, c2v, q, fs, w);
+            bit_planes(w, P);
+            const int nv = min(max(clen - 32 * k, 0), 32);
+            const uint32_t vmask = nv >= 32 ? 0xffffffffu : ((1u << nv) - 1u);
+            const uint32_t woff =
+                lane_off + (wide ? uint32_t((k >> 2) * 512 + (k & 3) * 4) : uint32_t(k * 4));
+            *reinterpret_cast<uint32_t*>(pm + woff) = 0u;  // code 0: the zero row
+            uint32_t hi_acc = 0u, hi_v = 0xffffffffu;
+#pragma unroll 1
+            for (uint32_t c = 1; c < sigma; ++c) {
+                const uint32_t v = inv[c];
+                if ((v >> 4) != hi_v) {  // warp-uniform: codes are sorted by byte value
+                    hi_v = v >> 4;
+                    hi_acc = ~((P[4] ^ (0u - ((v >> 4) & 1u))) | (P[5] ^ (0u - ((v >> 5) & 1u))) |
+                               (P[6] ^ (0u - ((v >> 6) & 1u))) | (P[7] ^ (0u - ((v >> 7) & 1u)))) &
+                             vmask;
+                }
+                const uint32_t m =
+                    hi_acc & ~((P[0] ^ (0u - (v & 1u))) | (P[1] ^ (0u - ((v >> 1) & 1u))) |
+                               (P[2] ^ (0u - ((v >> 2) & 1u))) | (P[3] ^ (0u - ((v >> 3) & 1u))));
+                *reinterpret_cast<uint32_t*>(pm + c * cs + woff) = m;
             }
+            c0v = c2v;
+            c1v = n1;
+            c2v = n2;
         }
     }
     __syncwarp();
