@@ -355,7 +355,7 @@ def run_c2(args, dist):
                    "global_batch": args.pairs * dist.world, "seq_len": "200-1000",
                    "parallelism": f"pair-sharded x{dist.world} (no collective)",
                    "cells_per_gpu_step": cells, "l2": "flushed between steps (300 MB write)"},
-        "gpu_launches": 3 * args.steps,
+        "gpu_launches": 4 * args.steps,  # plan, scan, scatter, main (CUB-free)
         "roofline": {"bound": "int", "achieved": round(achieved, 3), "peak": round(peak_t, 3),
                      "unit": "Tops/s (int32 ALU, 3 ops per 32-cell word-row)",
                      "frac": round(achieved / peak_t, 4), "traffic": None,
