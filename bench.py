@@ -408,13 +408,18 @@ def run_pair_config(args, dist):
         (lambda: wl.lcs_length(x, y, wl.NO_BUDGET))
     for _ in range(args.warmup):
         res = fn()
-    times = []
+    times, fill_ms = [], []
+    wl._check(wl.lib.wlcs_set_timing(1))
+    km = ctypes.c_float()
     with ClockSampler(dist.local_rank) as clocks:
         for _ in range(args.steps):
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             res = fn()
             times.append(time.perf_counter() - t0)
+            wl._check(wl.lib.wlcs_last_kernel_ms(ctypes.byref(km)))
+            fill_ms.append(km.value)
+    wl._check(wl.lib.wlcs_set_timing(0))
     t = float(np.mean(times))
     length = len(res) if sub else res
     return {"metric": METRIC, "value": round(cells / t / 1e9, 3), "unit": UNIT, "n_gpus": 1,
@@ -422,6 +427,9 @@ def run_pair_config(args, dist):
             "higher_is_better": True, "scaling": "none", "vs_baseline": None, "dtype": "u32",
             "data": "synthetic (paper_1306_4627_b200/workloads.py)",
             "config": {"workload": name, "lcs_length": length, "m": len(x), "n": len(y)},
+            "fill_kernel_ms": round(float(np.mean(fill_ms)), 3),
+            "fill_gcups": round(cells / (float(np.mean(fill_ms)) * 1e-3) / 1e9, 1)
+            if np.mean(fill_ms) > 0 else None,
             "clocks": clocks.summary(),
             "note": "end-to-end wall time through the C-ABI (H2D, fill, traceback, D2H)"}
 

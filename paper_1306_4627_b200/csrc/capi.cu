@@ -83,7 +83,7 @@ struct Ctx {
     // batch
     DevBuf xs, ys, xoff, yoff, out, ws;
     // single pair
-    DevBuf px, py, pmg, carry, small, rows, outrev;
+    DevBuf px, py, pmg, carry, small, rows, outrev, codes, ry, vbuf;
     ~Ctx() {
         if (stream) cudaStreamDestroy(stream);
     }
@@ -156,73 +156,133 @@ struct PairPlan {
     int K = 1;
 };
 
-int choose_k(const Ctx& c, int64_t W, int sigma, bool store) {
+// Words per lane.  Cost model (cycles ~ steps x per-row ALU ops): the fill
+// takes max(total strip-steps / resident warps, critical path) steps, where
+// the critical path is ~40 steps of hand-off skew per strip plus the rows of
+// one strip; a row costs ~3K+3 ALU ops.  Small K = more parallel strips but
+// more per-word overhead and a longer skew chain.
+int choose_k(const Ctx& c, int64_t W, int64_t rows_per_prob, int sigma, int nprob) {
     const int forced = env_int("WLCS_PAIR_K", 0);
     if (forced == 1 || forced == 2 || forced == 4 || forced == 8) return forced;
-    // Largest K whose strips still give every SM sub-partition a warp and
-    // whose match-mask slice fits comfortably in shared memory.
-    const int64_t target = int64_t(c.sms) * 4;
-    for (int K : {8, 4, 2}) {
-        const int64_t strips = (W + 32 * K - 1) / (32 * K);
-        if (strips >= target && wlcs::pair_smem_bytes(K, sigma) <= 96 * 1024) return K;
+    const double chunks = double((rows_per_prob + 15) / 16);
+    double best = 1e300;
+    int best_k = 1;
+    for (int K : {1, 2, 4, 8}) {
+        if (wlcs::pair_smem_bytes(K, sigma) > 200 * 1024) continue;
+        const double strips = double((W + 32 * K - 1) / (32 * K));
+        const double total = strips * nprob;
+        const double warps = std::min(total, 4.0 * c.sms);
+        const double steps = std::max(total * chunks / warps, strips * 40.0 + chunks);
+        const double cost = steps * (3.0 * K + 3.0);
+        if (cost < best) {
+            best = cost;
+            best_k = K;
+        }
     }
-    (void)store;
-    return 1;
+    return best_k;
 }
 
-// Prepares alphabet, match masks and buffers for the pair (row, col).
-int pair_setup(Ctx& c, const uint8_t* d_row, int64_t rows, const uint8_t* row_lo,
-               const uint8_t* row_hi, const uint8_t* d_col, int64_t cols, bool store,
-               PairPlan& plan) {
+void set_problem(wlcs::FillProblem& P, int64_t rows, uint32_t* pmg, int64_t cols, int K) {
+    P.rows = rows;
+    P.pmg = pmg;
+    P.cols = cols;
+    P.W = (cols + 31) / 32;
+    P.nstrips = int((P.W + 32 * K - 1) / (32 * K));
+    P.nchunks = int((rows + 15) / 16);
+    P.Mpad = int64_t(P.nchunks) * 16;
+    P.Dpad = P.Mpad + 512;
+}
+
+bool use_split(int64_t rows, bool store) {
+    if (store) return false;
+    const int forced = env_int("WLCS_PAIR_SPLIT", -1);
+    if (forced >= 0) return forced != 0 && rows >= 2;
+    return rows >= 2048;
+}
+
+// Prepares alphabet, match masks and buffers for the pair (row, col).  With
+// `split` the rows are cut in half and the bottom half runs on the reversed
+// strings as a second problem of the same launch (length only).
+// small: present[256] u32 @0 | map[256] u16 @1024 | sigma @1536 | ticket @1540 |
+//        zeros u64 @1544 | walk len u64 @1552 | safe16 @2048
+int pair_setup(Ctx& c, const uint8_t* d_row, int64_t rows, const uint8_t* d_col, int64_t cols,
+               bool store, PairPlan& plan) {
     wlcs::PairDev& d = plan.d;
-    d.rowp = d_row;
-    d.rows = rows;
-    d.row_lo = row_lo;
-    d.row_hi = row_hi;
-    d.colp = d_col;
-    d.cols = cols;
-    d.W = (cols + 31) / 32;
-    // small: present[256] u32 | map[256] u16 | sigma u32 | ticket | zeros u64 | walk len u64
+    const bool split = use_split(rows, store);
+    d.nprob = split ? 2 : 1;
+    d.colp0 = d_col;
+    d.prob[0].cols = cols;
     WLCS_CUDA(c.small.ensure(4096));
     uint8_t* sb = c.small.as<uint8_t>();
     uint32_t* present = reinterpret_cast<uint32_t*>(sb);
     uint16_t* map = reinterpret_cast<uint16_t*>(sb + 1024);
     uint32_t* sigma_dev = reinterpret_cast<uint32_t*>(sb + 1536);
     d.ticket = reinterpret_cast<uint32_t*>(sb + 1540);
-    d.zeros = reinterpret_cast<unsigned long long*>(sb + 1544);
+    unsigned long long* zeros = reinterpret_cast<unsigned long long*>(sb + 1544);
     d.safe16 = reinterpret_cast<const uint4*>(sb + 2048);  // zeroed below
     int sigma = 0;
     WLCS_CUDA(wlcs::pair_prepare(d, present, map, sigma_dev, c.stream, &sigma));
-    plan.K = choose_k(c, d.W, sigma, store);
-    if (wlcs::pair_smem_bytes(plan.K, sigma) > 220 * 1024) plan.K = 1;
+    const int64_t W = (cols + 31) / 32;
+    const int64_t mid = split ? rows / 2 : rows;
+    plan.K = choose_k(c, W, rows - mid > mid ? rows - mid : mid, sigma, d.nprob);
+    if (wlcs::pair_smem_bytes(plan.K, sigma) > 220 * 1024)
+        return fail(WLCS_E_INTERNAL, "match-mask table does not fit in shared memory");
     const int K = plan.K;
-    d.nstrips = int((d.W + 32 * K - 1) / (32 * K));
-    const int a_r = int(reinterpret_cast<uintptr_t>(d_row) & 15u);
-    d.nchunks = int((rows + a_r + 15) / 16);
-    WLCS_CUDA(c.pmg.ensure(size_t(sigma) * size_t(d.W) * 4));
-    d.pmg = c.pmg.as<uint32_t>();
-    const size_t carry_bytes = size_t(d.nstrips) * size_t(d.nchunks) * 4;
-    const size_t prog_bytes = (size_t(d.nstrips) * 4 + 255) & ~size_t(255);
-    WLCS_CUDA(c.carry.ensure(prog_bytes + carry_bytes));
-    d.progress = c.carry.as<uint32_t>();
-    d.carry = reinterpret_cast<uint32_t*>(c.carry.as<uint8_t>() + prog_bytes);
-    WLCS_CUDA(cudaMemsetAsync(d.progress, 0, prog_bytes, c.stream));
-    WLCS_CUDA(cudaMemsetAsync(d.ticket, 0, 4 + 4 + 8, c.stream));
-    WLCS_CUDA(cudaMemsetAsync(sb + 2048, 0, 16, c.stream));
-    d.Mpad = (rows + 15) & ~int64_t(15);
-    d.rows_out = nullptr;
-    if (store) {
-        const size_t bytes = size_t(d.nstrips) * 32 * size_t(d.Mpad) * size_t(K) * 4;
-        WLCS_CUDA(c.rows.ensure(bytes));
-        d.rows_out = c.rows.as<uint32_t>();
+    const size_t pm_words = size_t(sigma) * size_t(W);
+    WLCS_CUDA(c.pmg.ensure(pm_words * 4 * size_t(d.nprob)));
+    uint32_t* pmg = c.pmg.as<uint32_t>();
+    set_problem(d.prob[0], mid, pmg, cols, K);
+    if (split) {
+        set_problem(d.prob[1], rows - mid, pmg + pm_words, cols, K);
+        WLCS_CUDA(c.ry.ensure(size_t(cols) + 16));
+        WLCS_CUDA(c.vbuf.ensure(size_t(W) * 16 + 64));
+        WLCS_CUDA(wlcs::pair_reverse(d_col, cols, c.ry.as<uint8_t>(), c.stream));
+        d.prob[0].v_out = c.vbuf.as<uint32_t>();
+        d.prob[1].v_out = c.vbuf.as<uint32_t>() + W;
+    } else {
+        d.prob[0].zeros = zeros;
     }
-    WLCS_CUDA(wlcs::pair_build_pm(d, c.stream));
+    // pre-coded rows, padded on both sides (pair_code_rows)
+    size_t code_vecs = 0;
+    for (int q = 0; q < d.nprob; ++q) code_vecs += 4 * size_t(wlcs::pair_code_plane(d.prob[q].nchunks));
+    WLCS_CUDA(c.codes.ensure(code_vecs * 16));
+    uint4* code_base = c.codes.as<uint4>();
+    for (int q = 0; q < d.nprob; ++q) {
+        const uint8_t* src = q == 0 ? d_row : d_row + mid;
+        WLCS_CUDA(wlcs::pair_code_rows(src, d.prob[q].rows, q == 1, map, K, d.prob[q], code_base,
+                                       c.stream));
+        code_base += 4 * wlcs::pair_code_plane(d.prob[q].nchunks);
+    }
+    size_t carry_words = 0;
+    for (int q = 0; q < d.nprob; ++q)
+        carry_words += size_t(d.prob[q].nstrips) * size_t(d.prob[q].nchunks);
+    WLCS_CUDA(c.carry.ensure(carry_words * 4 + 256));
+    uint32_t* carry = c.carry.as<uint32_t>();
+    for (int q = 0; q < d.nprob; ++q) {
+        d.prob[q].carry = carry;
+        carry += size_t(d.prob[q].nstrips) * size_t(d.prob[q].nchunks);
+    }
+    WLCS_CUDA(cudaMemsetAsync(c.carry.p, 0, carry_words * 4, c.stream));
+    WLCS_CUDA(cudaMemsetAsync(d.ticket, 0, 4 + 4 + 8 + 8, c.stream));
+    WLCS_CUDA(cudaMemsetAsync(sb + 2048, 0, 16, c.stream));
+    if (store) {
+        const size_t bytes =
+            size_t(d.prob[0].nstrips) * 32 * size_t(d.prob[0].Dpad) * size_t(K) * 4;
+        WLCS_CUDA(c.rows.ensure(bytes));
+        d.prob[0].rows_out = c.rows.as<uint32_t>();
+    }
+    WLCS_CUDA(wlcs::pair_build_pm(d_col, cols, map, sigma, W, pmg, c.stream));
+    if (split) WLCS_CUDA(wlcs::pair_build_pm(c.ry.as<uint8_t>(), cols, map, sigma, W,
+                                             pmg + pm_words, c.stream));
     return WLCS_OK;
 }
 
+unsigned long long* pair_zeros_ptr(Ctx& c) {
+    return reinterpret_cast<unsigned long long*>(c.small.as<uint8_t>() + 1544);
+}
+
 int pair_length_device(Ctx& c, const uint8_t* dx, size_t m, const uint8_t* dy, size_t n,
-                       const uint8_t* x_lo, const uint8_t* x_hi, const uint8_t* y_lo,
-                       const uint8_t* y_hi, uint32_t* out) {
+                       uint32_t* out) {
     if (m == 0 || n == 0) {
         *out = 0;
         return WLCS_OK;
@@ -231,14 +291,28 @@ int pair_length_device(Ctx& c, const uint8_t* dx, size_t m, const uint8_t* dy, s
     // sequential dimension is short and the parallel (strip) dimension wide.
     const bool x_rows = m <= n;
     PairPlan plan;
-    int rc = x_rows ? pair_setup(c, dx, int64_t(m), x_lo, x_hi, dy, int64_t(n), false, plan)
-                    : pair_setup(c, dy, int64_t(n), y_lo, y_hi, dx, int64_t(m), false, plan);
+    int rc = x_rows ? pair_setup(c, dx, int64_t(m), dy, int64_t(n), false, plan)
+                    : pair_setup(c, dy, int64_t(n), dx, int64_t(m), false, plan);
     if (rc) return rc;
+    if (c.timing && !c.ev0) {
+        WLCS_CUDA(cudaEventCreate(&c.ev0));
+        WLCS_CUDA(cudaEventCreate(&c.ev1));
+    }
+    if (c.timing) WLCS_CUDA(cudaEventRecord(c.ev0, c.stream));
     WLCS_CUDA(wlcs::pair_fill(plan.d, plan.K, false, c.sms, c.stream));
-    unsigned long long zeros = 0;
-    WLCS_CUDA(cudaMemcpyAsync(&zeros, plan.d.zeros, 8, cudaMemcpyDeviceToHost, c.stream));
+    if (c.timing) WLCS_CUDA(cudaEventRecord(c.ev1, c.stream));
+    unsigned long long* zeros = pair_zeros_ptr(c);
+    if (plan.d.nprob == 2) {
+        const wlcs::FillProblem& P = plan.d.prob[0];
+        uint32_t* scratch = c.vbuf.as<uint32_t>() + 2 * P.W;
+        WLCS_CUDA(wlcs::pair_split_combine(P.v_out, plan.d.prob[1].v_out, P.W, P.cols, scratch,
+                                           zeros, c.stream));
+    }
+    unsigned long long len = 0;
+    WLCS_CUDA(cudaMemcpyAsync(&len, zeros, 8, cudaMemcpyDeviceToHost, c.stream));
     WLCS_CUDA(cudaStreamSynchronize(c.stream));
-    *out = uint32_t(zeros);
+    if (c.timing) WLCS_CUDA(cudaEventElapsedTime(&c.last_main_ms, c.ev0, c.ev1));
+    *out = uint32_t(len);
     return WLCS_OK;
 }
 
@@ -287,8 +361,7 @@ int batch_device(Ctx& c, const uint8_t* d_xs, const uint64_t* d_xoff, const uint
         WLCS_CUDA(cudaMemcpy(yo, d_yoff + p, 16, cudaMemcpyDeviceToHost));
         uint32_t len = 0;
         int rc = pair_length_device(c, d_xs + xo[0], size_t(xo[1] - xo[0]), d_ys + yo[0],
-                                    size_t(yo[1] - yo[0]), d_xs, d_xs + xs_bytes, d_ys,
-                                    d_ys + ys_bytes, &len);
+                                    size_t(yo[1] - yo[0]), &len);
         if (rc) return rc;
         WLCS_CUDA(cudaMemcpy(d_out + p, &len, 4, cudaMemcpyHostToDevice));
     }
@@ -346,7 +419,7 @@ int wlcs_length_ex(const uint8_t* x, size_t m, const uint8_t* y, size_t n, size_
     WLCS_CUDA(cudaMemcpyAsync(c->py.p, y, n, cudaMemcpyHostToDevice, c->stream));
     const uint8_t* dx = c->px.as<uint8_t>();
     const uint8_t* dy = c->py.as<uint8_t>();
-    return pair_length_device(*c, dx, m, dy, n, dx, dx + m, dy, dy + n, out);
+    return pair_length_device(*c, dx, m, dy, n, out);
 }
 
 int wlcs_length(const uint8_t* x, size_t m, const uint8_t* y, size_t n, size_t memory_budget,
@@ -366,7 +439,7 @@ int wlcs_length_device(const uint8_t* d_x, size_t m, const uint8_t* d_y, size_t 
     if (variant != WLCS_VARIANT_BITPARALLEL)
         return fail(WLCS_E_CONFIG, "fill variant " + std::to_string(variant) +
                                        " is not available for single pairs");
-    return pair_length_device(*c, d_x, m, d_y, n, d_x, d_x + m, d_y, d_y + n, out);
+    return pair_length_device(*c, d_x, m, d_y, n, out);
 }
 
 int wlcs_subsequence(const uint8_t* x, size_t m, const uint8_t* y, size_t n,
@@ -388,17 +461,25 @@ int wlcs_subsequence(const uint8_t* x, size_t m, const uint8_t* y, size_t n,
     const uint8_t* dy = c->py.as<uint8_t>();
     // Orientation matters for tie-breaking: rows = x (parent), columns = y.
     PairPlan plan;
-    rc = pair_setup(*c, dx, int64_t(m), dx, dx + m, dy, int64_t(n), true, plan);
+    rc = pair_setup(*c, dx, int64_t(m), dy, int64_t(n), true, plan);
     if (rc) return rc;
+    if (c->timing && !c->ev0) {
+        WLCS_CUDA(cudaEventCreate(&c->ev0));
+        WLCS_CUDA(cudaEventCreate(&c->ev1));
+    }
+    if (c->timing) WLCS_CUDA(cudaEventRecord(c->ev0, c->stream));
     WLCS_CUDA(wlcs::pair_fill(plan.d, plan.K, true, c->sms, c->stream));
+    if (c->timing) WLCS_CUDA(cudaEventRecord(c->ev1, c->stream));
     const size_t maxlen = std::min(m, n);
     WLCS_CUDA(c->outrev.ensure(maxlen + 16));
-    unsigned long long* dlen = plan.d.zeros + 1;
+    unsigned long long* zeros_dev = pair_zeros_ptr(*c);
+    unsigned long long* dlen = zeros_dev + 1;
     WLCS_CUDA(wlcs::pair_walk(plan.d, plan.K, dx, c->outrev.as<uint8_t>(), dlen, c->stream));
     unsigned long long len = 0, zeros = 0;
     WLCS_CUDA(cudaMemcpyAsync(&len, dlen, 8, cudaMemcpyDeviceToHost, c->stream));
-    WLCS_CUDA(cudaMemcpyAsync(&zeros, plan.d.zeros, 8, cudaMemcpyDeviceToHost, c->stream));
+    WLCS_CUDA(cudaMemcpyAsync(&zeros, zeros_dev, 8, cudaMemcpyDeviceToHost, c->stream));
     WLCS_CUDA(cudaStreamSynchronize(c->stream));
+    if (c->timing) WLCS_CUDA(cudaEventElapsedTime(&c->last_main_ms, c->ev0, c->ev1));
     if (len != zeros)
         return fail(WLCS_E_INTERNAL, "traceback length " + std::to_string(len) +
                                          " differs from the fill length " + std::to_string(zeros));

@@ -41,32 +41,49 @@ uint32_t* batch_overflow_list_ptr(void* workspace, uint32_t pairs);
 
 namespace wlcs {
 
-// One pair for the strip kernel, all pointers DEVICE pointers.
-struct PairDev {
-    const uint8_t* rowp;    // row string (x for traceback; the shorter one for length)
+// One bit-parallel fill problem of the strip kernel (DEVICE pointers): all
+// rows of `coded` against the column string whose match masks are `pmg`.
+struct FillProblem {
+    const uint4* coded;     // pre-coded rows (pair_code_rows): plane 0, chunk 0
+    int64_t plane;          // uint4 stride between the 4 coded planes
+    int64_t cstride;        // uint4 stride between chunks
     int64_t rows;
-    const uint8_t* row_lo;  // allocation extent of the row string
-    const uint8_t* row_hi;
-    const uint8_t* colp;    // column (bit-vector) string
-    int64_t cols;
-    const uint16_t* map;    // 256 byte -> code map of the column alphabet
-    int sigma;              // codes incl. the zero row
     const uint32_t* pmg;    // global match masks [sigma][W]
     int64_t W;              // words per row = ceil(cols / 32)
+    int64_t cols;
     int nstrips;            // ceil(W / (32 K))
-    int nchunks;            // 16-row chunks of the row string (alignment included)
-    uint32_t* carry;        // [nstrips][nchunks] carry masks between strips
-    uint32_t* progress;     // [nstrips] published chunk counts
+    int nchunks;            // 16-row chunks of the row string
+    uint32_t* carry;        // [nstrips][nchunks] carry words, zero-initialised
+    uint32_t* v_out;        // optional: final V words [>= W]
+    unsigned long long* zeros;  // optional: LCS accumulator
+    uint32_t* rows_out;     // optional: bit rows, diagonal layout (traceback)
+    int64_t Mpad;           // nchunks * 16
+    int64_t Dpad;           // diagonals per strip in rows_out = Mpad + 512
+};
+
+// One strip-kernel launch: 1 or 2 problems sharing the column alphabet.
+struct PairDev {
+    FillProblem prob[2];
+    int nprob;
+    uint32_t code_stride;   // smem bytes per code record (set by pair_fill)
+    int carry_win;          // chunks per carry-word window (set by pair_fill)
+    const uint8_t* colp0;   // column string of problem 0 (alphabet scan)
+    const uint16_t* map;    // 256 byte -> code map of the column alphabet
+    int sigma;              // codes incl. the zero row
     uint32_t* ticket;       // strip ticket counter
-    unsigned long long* zeros;  // LCS accumulator
-    uint32_t* rows_out;     // optional: bit rows [G][Mpad][K]
-    int64_t Mpad;
     const uint4* safe16;    // 16 zero bytes in device memory
 };
 
 cudaError_t pair_prepare(PairDev& d, uint32_t* present256, uint16_t* map256, uint32_t* sigma_dev,
                          cudaStream_t stream, int* sigma_host);
-cudaError_t pair_build_pm(const PairDev& d, cudaStream_t stream);
+cudaError_t pair_build_pm(const uint8_t* colp, int64_t cols, const uint16_t* map, int sigma,
+                          int64_t W, uint32_t* pmg, cudaStream_t stream);
+int64_t pair_code_plane(int nchunks);  // uint4 entries per coded plane (with padding)
+cudaError_t pair_code_rows(const uint8_t* row, int64_t rows, bool reverse, const uint16_t* map,
+                           int K, FillProblem& P, uint4* coded_base, cudaStream_t stream);
+cudaError_t pair_reverse(const uint8_t* src, int64_t n, uint8_t* dst, cudaStream_t stream);
+cudaError_t pair_split_combine(const uint32_t* vf, const uint32_t* vr, int64_t W, int64_t N,
+                               uint32_t* scratch, unsigned long long* best, cudaStream_t stream);
 int pair_smem_bytes(int K, int sigma);
 cudaError_t pair_fill(const PairDev& d, int K, bool store, int sms, cudaStream_t stream);
 cudaError_t pair_walk(const PairDev& d, int K, const uint8_t* x, uint8_t* out_rev,
