@@ -118,6 +118,14 @@ __device__ __forceinline__ uint32_t ld_relaxed_gpu(const uint32_t* p) {
     asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
+__device__ __forceinline__ uint4 ld_relaxed_gpu_v4(const uint32_t* p) {
+    uint4 v;
+    asm volatile("ld.relaxed.gpu.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p)
+                 : "memory");
+    return v;
+}
 __device__ __forceinline__ void st_relaxed_gpu(uint32_t* p, uint32_t v) {
     asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -134,7 +142,12 @@ constexpr int kPairWarps = 4;               // max warps per CTA
 // 4j..4j+3 of every chunk, chunk ch at index ch + kPadChunks, so the warp's
 // j-th LDG.128 (lanes on chunks t-0 .. t-31) is one contiguous 512-byte run.
 // With `reverse` the row string is coded back to front.
-constexpr int kPadChunks = 32;
+constexpr int kPadChunks = 40;  // >= 31 (lane skew) + 3 (group rounding) + kCodeAhead
+constexpr int kCodeAhead = 4;   // code prefetch distance in steps
+
+struct Codes {
+    uint4 a, b, c, d;  // rows 0-3, 4-7, 8-11, 12-15 of a chunk
+};
 
 __global__ void pair_code_rows_kernel(const uint8_t* row, int64_t rows, int reverse,
                                       const uint16_t* map, int64_t plane, int64_t cstride,
@@ -155,23 +168,21 @@ __global__ void pair_code_rows_kernel(const uint8_t* row, int64_t rows, int reve
 // t / nprob), so inside each problem strips start in order and a strip only
 // ever waits on a strip that is already running.
 //
-// Per step a lane reads its 16-row chunk as 16 pre-coded offsets (4
-// coalesced LDG.128, prefetched one step ahead) and runs 16 row updates: per row one IADD3 for
-// the address, one LDS for the masks, 3 ALU ops per word plus two for the
-// carry bit in and out.
+// Per step a lane reads its 16-row chunk as 16 codes (4 coalesced LDG.128,
+// prefetched kCodeAhead steps ahead) and runs 16 row updates: per row one
+// IMAD for the mask address, one LDS, 3 ALU ops per word plus one ALU op and
+// one IMAD.X for the carry bit in and out.
 //
 // Carry handoff between strips: lane 31 of strip s publishes the 16-row carry
 // mask of chunk ch as one relaxed 32-bit store (kCarryValid | mask) into a
 // zero-initialised buffer -- the data word is its own ready flag, so no fence
-// is needed.  Strip s+1 reads the words in windows, the
-// next window prefetched while the current one is consumed (`win` chunks, 16 by default); a word that was
-// still 0 when loaded is re-polled.  (A per-step ring refill was tried: its
-// pending load blocks the next step's shuffle of the ring register.)
+// is needed.  Lane 0 of strip s+1 reads the words four chunks at a time (one
+// 16-byte relaxed load), one group of four steps ahead; a word that was still
+// 0 when loaded is re-polled.  Inside the warp the carry masks move with two
+// shuffles per step (rows 0-7 after row 7, rows 8-15 after row 15), so the
+// shuffle latency hides behind row work.
 //
-// CTAs are persistent with kPairWarps independent warps, one per SM
-// sub-partition, so no strip shares an ALU pipe with another strip (a strip
-// on a shared sub-partition would run at half speed and throttle every strip
-// downstream of it).
+// Launch: 1-warp CTAs by default (WLCS_PAIR_WPC selects up to kPairWarps).
 template <int K, bool STORE>
 __global__ void __launch_bounds__(32 * kPairWarps) pair_strip_kernel(PairDev d) {
     extern __shared__ __align__(16) uint8_t smem[];
@@ -205,66 +216,85 @@ __global__ void __launch_bounds__(32 * kPairWarps) pair_strip_kernel(PairDev d) 
         for (int k = 0; k < K; ++k) V[k] = 0xffffffffu;
         const bool has_left = strip > 0;
         const bool has_right = strip + 1 < uint32_t(P.nstrips);
-        const uint32_t* left_carry = P.carry + int64_t(has_left ? strip - 1 : 0) * nchunks;
-        uint32_t* my_carry = P.carry + int64_t(strip) * nchunks;
-        const int win = d.carry_win;
-        // carry windows of `win` chunks: lanes 0..win-1 hold the words
-        // of the current window (cur_in) and of the next one (nxt_in)
-        auto carry_word = [&](int ch) -> uint32_t {
-            return (has_left && int(lane) < win && ch < nchunks)
-                       ? ld_relaxed_gpu(left_carry + ch)
-                       : kCarryValid;
-        };
-        uint32_t cur_in = carry_word(int(lane)), nxt_in = carry_word(win + int(lane));
-        uint32_t cout = 0;
+        const int64_t cwords = P.cwords;  // carry-row stride (multiple of 4)
+        const uint32_t* left_carry = P.carry + int64_t(has_left ? strip - 1 : 0) * cwords;
+        uint32_t* my_carry = P.carry + int64_t(strip) * cwords;
+        const bool feeder = has_left && lane == 0;
+        // lane 0 reads the left strip's carry words four chunks at a time, one
+        // group ahead (words past nchunks are never written and stay 0)
+        uint4 cw = make_uint4(0, 0, 0, 0), cw_next = cw;
+        if (feeder) cw_next = ld_relaxed_gpu_v4(left_carry);
         StoreHook<K, STORE> hook{
             STORE ? P.rows_out + ((int64_t(strip) * P.Dpad) * 32 + lane) * K : nullptr, 0};
-        const int T = nchunks + 31;
+        const int T = (nchunks + 31 + 3) & ~3;
         // lane l works on chunk t - l (chunks < 0 / >= nchunks are padding);
-        // codes are prefetched two steps ahead
+        // codes are prefetched kCodeAhead steps ahead: lane 0's chunk is always
+        // new data (an L2 round trip), the other lanes re-read lane l-1's chunk
         const int64_t cstride = P.cstride;
         const uint4* cp = P.coded - int64_t(lane) * cstride;
-        uint4 a0 = __ldg(cp), a1 = __ldg(cp + plane), a2 = __ldg(cp + 2 * plane),
-              a3 = __ldg(cp + 3 * plane);
-        cp += cstride;
-        uint4 b0 = __ldg(cp), b1 = __ldg(cp + plane), b2 = __ldg(cp + 2 * plane),
-              b3 = __ldg(cp + 3 * plane);
+        auto load_codes = [&](const uint4* q) {
+            return Codes{__ldg(q), __ldg(q + plane), __ldg(q + 2 * plane), __ldg(q + 3 * plane)};
+        };
+        Codes r0 = load_codes(cp), r1 = load_codes(cp + cstride),
+              r2 = load_codes(cp + 2 * cstride), r3 = load_codes(cp + 3 * cstride);
+        cp += kCodeAhead * cstride;
         const uint8_t* pml = pm + lane_off;
         const uint32_t csr = d.code_stride;  // runtime value: address IMAD stays on the FMA pipe
-        for (int t = 0; t < T; ++t) {
-            uint32_t from_left = 0;
-            if (has_left && t < nchunks) {
-                if ((t & (win - 1)) == 0) {
-                    if (t > 0) {
-                        cur_in = nxt_in;
-                        nxt_in = carry_word(t + win + int(lane));
-                    }
-                    // wait for the current window (normally already published)
-                    while (__any_sync(kFullMask, cur_in == 0u))
-                        if (cur_in == 0u) cur_in = carry_word(t + int(lane));
-                }
-                from_left = __shfl_sync(kFullMask, cur_in, t & (win - 1));
-            }
-            const int ch = t - int(lane);
-            cp += cstride;
-            const uint4 n0 = __ldg(cp), n1 = __ldg(cp + plane), n2 = __ldg(cp + 2 * plane),
-                        n3 = __ldg(cp + 3 * plane);
-            uint32_t cin = __shfl_up_sync(kFullMask, cout, 1);
-            if (lane == 0) cin = from_left & 0xffffu;
-            cin <<= 16;
-            cout = 0;
-            const uint32_t code[16] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w,
-                                       a2.x, a2.y, a2.z, a2.w, a3.x, a3.y, a3.z, a3.w};
-            if constexpr (STORE) hook.dlo = int64_t(t) * 16;
-            const bool valid = ch >= 0 && ch < nchunks;
+        // carry-in masks of the current step, rows 0-7 / 8-15 at bits 31..24
+        // (consumed MSB first); the shuffles of a step's carry-outs are issued
+        // mid-step and at step end so their latency hides behind row work
+        uint32_t cin_lo = 0, cin_hi = 0;
+        for (int tg = 0; tg < T; tg += 4) {
+            if (feeder && tg < nchunks) {
+                cw = cw_next;
+                uint32_t* w = &cw.x;
 #pragma unroll
-            for (int r = 0; r < 16; ++r) {
-                row_update<true, K>(V, pml, code[r] * csr, cin, cout);
-                hook(r, valid, V);
+                for (int j = 0; j < 4; ++j)
+                    while (tg + j < nchunks && w[j] == 0u) w[j] = ld_relaxed_gpu(left_carry + tg + j);
+                cw_next = ld_relaxed_gpu_v4(left_carry + tg + 4);
             }
-            if (has_right && lane == 31 && valid) st_relaxed_gpu(my_carry + ch, kCarryValid | cout);
-            a0 = b0; a1 = b1; a2 = b2; a3 = b3;
-            b0 = n0; b1 = n1; b2 = n2; b3 = n3;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int t = tg + j;
+                const int ch = t - int(lane);
+                const Codes nx = load_codes(cp);
+                cp += cstride;
+                if (lane == 0) {
+                    uint32_t fl = j == 0 ? cw.x : j == 1 ? cw.y : j == 2 ? cw.z : cw.w;
+                    if (t >= nchunks) fl = 0;  // padding rows take no carry
+                    cin_lo = (fl & 0xff00u) << 16;
+                    cin_hi = (fl & 0xffu) << 24;
+                }
+                const uint32_t code[16] = {r0.a.x, r0.a.y, r0.a.z, r0.a.w, r0.b.x, r0.b.y,
+                                           r0.b.z, r0.b.w, r0.c.x, r0.c.y, r0.c.z, r0.c.w,
+                                           r0.d.x, r0.d.y, r0.d.z, r0.d.w};
+                if constexpr (STORE) hook.dlo = int64_t(t) * 16;
+                const bool valid = ch >= 0 && ch < nchunks;
+                uint32_t Pm[16][K];
+#pragma unroll
+                for (int r = 0; r < 16; ++r) load_pm<K>(pml, code[r] * csr, Pm[r]);
+                uint32_t cout_lo = 0, cout_hi = 0;
+#pragma unroll
+                for (int r = 0; r < 8; ++r) {
+                    RowStep<K>::chain(V, Pm[r], cin_lo, cout_lo);
+                    hook(r, valid, V);
+                }
+                const uint32_t nl = __shfl_up_sync(kFullMask, cout_lo, 1);
+#pragma unroll
+                for (int r = 8; r < 16; ++r) {
+                    RowStep<K>::chain(V, Pm[r], cin_hi, cout_hi);
+                    hook(r, valid, V);
+                }
+                const uint32_t nh = __shfl_up_sync(kFullMask, cout_hi, 1);
+                if (has_right && lane == 31 && valid)
+                    st_relaxed_gpu(my_carry + ch, kCarryValid | (cout_lo << 8) | cout_hi);
+                cin_lo = nl << 24;
+                cin_hi = nh << 24;
+                r0 = r1;
+                r1 = r2;
+                r2 = r3;
+                r3 = nx;
+            }
         }
         if (P.v_out) {
 #pragma unroll
@@ -280,44 +310,188 @@ __global__ void __launch_bounds__(32 * kPairWarps) pair_strip_kernel(PairDev d) 
     }
 }
 
-// Exact reference traceback over stored bit rows (one thread).
+// Exact reference traceback over stored bit rows, one warp.
 // out receives the subsequence in REVERSE order; *out_len its length.
+//
+// The walk is sequential (row i's decision sets the column for row i-1) and
+// latency-bound.  The warp works in blocks of 32 rows: every lane prepares,
+// for one row, a window of kWalkWords words at and below a predicted column
+// word in shared memory -- the event bits E = PM | ~V (match or Up), the
+// match bits PM, and for each word the position/type of the highest event
+// in the words below it -- so that lane 0's per-row step is three independent
+// LDS plus a handful of 32-bit ALU ops, with no data-dependent loop.  The
+// preparation of block b+1 is issued before lane 0 walks block b, so the
+// DRAM latency of the bit rows overlaps the walk.  A row whose next event
+// lies below the window is searched in global memory (rare).
+constexpr int kWalkWords = 8;
+
 template <int K>
-__global__ void pair_walk_kernel(PairDev d, const uint8_t* x, uint8_t* out,
-                                 unsigned long long* out_len) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    const FillProblem& P = d.prob[0];
-    int64_t i = P.rows, j = P.cols;  // 1-based DP coordinates
-    unsigned long long len = 0;
-    const int64_t W = P.W;
-    while (i > 0 && j > 0) {
-        const int64_t q = i - 1;  // string index of row i
-        const uint32_t code = d.map[x[q]];
-        const uint32_t* pmrow = P.pmg + int64_t(code) * W;
-        int64_t w = (j - 1) >> 5;
-        int b = int((j - 1) & 31);
-        uint32_t v = P.rows_out[pair_row_index(q, w, K, P.Dpad)];
-        uint32_t pmw = __ldg(pmrow + w);
-        uint32_t e = (pmw | ~v) & (b == 31 ? 0xffffffffu : ((2u << b) - 1u));
-        while (e == 0 && w > 0) {
-            --w;
-            v = P.rows_out[pair_row_index(q, w, K, P.Dpad)];
-            pmw = __ldg(pmrow + w);
-            e = pmw | ~v;
+__device__ __noinline__ int64_t walk_row_global(const FillProblem& P, const uint16_t* map,
+                                                uint8_t xq, int64_t q, int64_t j, bool* diag) {
+    int64_t w = (j - 1) >> 5;
+    const uint32_t* pmrow = P.pmg + int64_t(map[xq]) * P.W;
+    uint32_t mask = (2u << ((j - 1) & 31)) - 1u;
+    for (;; --w, mask = 0xffffffffu) {
+        const uint32_t pmw = __ldg(pmrow + w);
+        const uint32_t e = (pmw | ~P.rows_out[pair_row_index(q, w, K, P.Dpad)]) & mask;
+        if (e) {
+            const int b = 31 - __clz(e);
+            *diag = (pmw >> b) & 1u;
+            return w * 32 + b + 1 - (*diag ? 1 : 0);
         }
-        if (e == 0) break;  // Left all the way to column 0
-        b = 31 - __clz(e);
-        const int64_t jj = w * 32 + b + 1;  // event column
-        if ((pmw >> b) & 1u) {
-            out[len++] = x[q];
-            i -= 1;
-            j = jj - 1;
-        } else {
-            i -= 1;
-            j = jj;
+        if (w == 0) {
+            *diag = false;
+            return 0;  // Left all the way to column 0
         }
     }
-    *out_len = len;
+}
+
+template <int K>
+__global__ void __launch_bounds__(32) pair_walk_kernel(PairDev d, const uint8_t* x, uint8_t* out,
+                                                       unsigned long long* out_len) {
+    __shared__ uint32_t se[2][32][kWalkWords], sp[2][32][kWalkWords];
+    __shared__ int32_t sv[2][32][kWalkWords];  // (pos*2 + diag) of the highest event below word s
+    __shared__ uint8_t sx[2][32];
+    const FillProblem& P = d.prob[0];
+    const int lane = int(threadIdx.x);
+    const int64_t W = P.W;
+    // match masks: the whole table in shared memory when it fits (pm_smem)
+    extern __shared__ __align__(16) uint32_t spm[];
+    const bool pm_smem = d.walk_pm_smem != 0;
+    if (pm_smem) {
+        for (int64_t k = lane; k < int64_t(d.sigma) * W; k += 32) spm[k] = __ldg(P.pmg + k);
+        __syncwarp();
+    }
+    auto pm_word = [&](uint32_t code, int64_t w) -> uint32_t {
+        return pm_smem ? spm[int64_t(code) * W + w] : __ldg(P.pmg + int64_t(code) * W + w);
+    };
+    // stage 1 (before lane 0 walks the current block): the row byte, its code
+    // and the raw V words of row ibase-1-lane, words wlo .. wlo+7 -- loads
+    // only, nothing consumes them until stage 2
+    uint32_t rv[kWalkWords];
+    uint32_t rcode = 0;
+    uint8_t rx = 0;
+    const uint32_t* coded32 = reinterpret_cast<const uint32_t*>(P.coded);
+    auto fetch = [&](int64_t ibase, int64_t wlo) {
+        const int64_t q = ibase - 1 - lane;
+        rcode = 0;
+#pragma unroll
+        for (int s = 0; s < kWalkWords; ++s) rv[s] = 0xffffffffu;
+        if (q >= 0) {
+            rx = x[q];
+            const int64_t r = q & 15, ch = q >> 4;
+            rcode = coded32[((r >> 2) * P.plane + ch * P.cstride) * 4 + (r & 3)];
+#pragma unroll
+            for (int s = 0; s < kWalkWords; ++s) {
+                const int64_t w = wlo + s;
+                if (w < W) rv[s] = P.rows_out[pair_row_index(q, w, K, P.Dpad)];
+            }
+        }
+    };
+    // stage 2: event words, match words and the below-word summaries
+    auto commit = [&](int buf, int64_t wlo) {
+        int32_t prev = -1;
+#pragma unroll
+        for (int s = 0; s < kWalkWords; ++s) {
+            const int64_t w = wlo + s;
+            const uint32_t pm = w < W ? pm_word(rcode, w) : 0u;
+            const uint32_t ev = pm | ~rv[s];
+            se[buf][lane][s] = ev;
+            sp[buf][lane][s] = pm;
+            sv[buf][lane][s] = prev;
+            if (ev) {
+                const int b = 31 - __clz(ev);
+                prev = (s * 32 + b) * 2 + int((pm >> b) & 1u);
+            }
+        }
+        sx[buf][lane] = rx;
+    };
+    int64_t i = P.rows, j = P.cols;  // 1-based DP coordinates
+    unsigned long long len = 0;
+    int buf = 0;
+    // window: the kWalkWords words at and below the column word at fetch time
+    // (j only decreases; 256 columns cover the drop over this block and the
+    // next one for any path that is not a long run of Left moves)
+    auto window_lo = [&](int64_t jtop) {
+        const int64_t lo = ((jtop - 1) >> 5) - (kWalkWords - 1);
+        return lo < 0 ? int64_t(0) : lo;
+    };
+    int64_t wlo = window_lo(j);
+    if (i > 0 && j > 0) {
+        fetch(i, wlo);
+        commit(0, wlo);
+    }
+    __syncwarp();
+    while (i > 0 && j > 0) {
+        const int64_t wlo_next = window_lo(j);
+        fetch(i - 32, wlo_next);
+        if (lane == 0) {
+            const int rows = i < 32 ? int(i) : 32;
+            const int64_t jbase = 32 * wlo;
+            int32_t jl = int32_t(j - jbase);  // local column, 1 .. 32*kWalkWords
+            uint8_t* o = out + len;
+            int n = 0;
+            int l = 0;
+            bool ended = false;
+            // one row; returns false when the walk has ended
+            auto step = [&](int r) -> bool {
+                const int32_t jm = jl - 1;
+                const int sw = jm >> 5;  // < 0: below the window (rare path)
+                const int sc = sw < 0 ? 0 : sw;
+                const uint32_t e = se[buf][r][sc] & ((2u << (jm & 31)) - 1u);
+                const uint32_t pw = sp[buf][r][sc];
+                const int32_t pv = sv[buf][r][sc];
+                const int b = 31 - __clz(e);
+                int32_t pos = e ? sc * 32 + b : pv >> 1;
+                int32_t dg = e ? int32_t((pw >> b) & 1u) : (pv & 1);
+                if (sw < 0 || (e == 0u && pv < 0)) {  // rare: below the window or no event
+                    if (jbase + jl <= 0) return false;  // column 0: the walk has ended
+                    if (wlo == 0 && sw >= 0) {          // no event down to column 0
+                        jl = int32_t(-jbase);
+                        return false;
+                    }
+                    const int64_t jq = sw < 0 ? jbase + jl : jbase + 32 * sc;
+                    bool dgb = false;
+                    const int64_t jn = walk_row_global<K>(P, d.map, sx[buf][r], i - 1 - r, jq, &dgb);
+                    pos = int32_t(jn - jbase) - (dgb ? 0 : 1);
+                    dg = dgb ? 1 : 0;
+                }
+                o[n] = sx[buf][r];  // kept only if dg (the next emit overwrites it)
+                n += dg;
+                jl = pos + 1 - dg;
+                return true;
+            };
+            if (rows == 32) {
+#pragma unroll
+                for (int r = 0; r < 32; ++r) {
+                    if (!step(r)) {
+                        ended = true;
+                        l = r + 1;
+                        break;
+                    }
+                }
+                if (!ended) l = 32;
+            } else {
+                for (; l < rows; ++l) {
+                    if (!step(l)) {
+                        ++l;
+                        break;
+                    }
+                }
+            }
+            len += n;
+            j = jbase + jl;
+            if (j < 0) j = 0;
+            i -= l;
+        }
+        i = __shfl_sync(kFullMask, i, 0);
+        j = __shfl_sync(kFullMask, j, 0);
+        buf ^= 1;
+        wlo = wlo_next;
+        commit(buf, wlo);
+        __syncwarp();
+    }
+    if (lane == 0) *out_len = len;
 }
 
 // ---- bidirectional split (Hirschberg's lemma) -----------------------------
@@ -473,14 +647,12 @@ cudaError_t pair_code_rows(const uint8_t* row, int64_t rows, bool reverse, const
 template <int K, bool STORE>
 static cudaError_t launch_strip(const PairDev& d, int sms, cudaStream_t stream) {
     const_cast<PairDev&>(d).code_stride = uint32_t(pair_code_stride(K));
-    const char* wenv = std::getenv("WLCS_PAIR_WIN");
-    int win = wenv && *wenv ? std::atoi(wenv) : 16;
-    if (win != 4 && win != 8 && win != 16 && win != 32) win = 16;
-    const_cast<PairDev&>(d).carry_win = win;
     const char* env = std::getenv("WLCS_PAIR_WPC");
     int wpc = env && *env ? std::atoi(env) : 1;
     if (wpc < 1 || wpc > kPairWarps) wpc = 1;
-    const int smem = wpc * pair_smem_bytes(K, d.sigma);
+    int smem = wpc * pair_smem_bytes(K, d.sigma);
+    const char* solo = std::getenv("WLCS_PAIR_SOLO");
+    if (solo && *solo == '1' && smem < 116 * 1024) smem = 116 * 1024;  // one CTA per SM
     cudaError_t e = cudaFuncSetAttribute(pair_strip_kernel<K, STORE>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
@@ -512,14 +684,24 @@ cudaError_t pair_fill(const PairDev& d, int K, bool store, int sms, cudaStream_t
 
 cudaError_t pair_walk(const PairDev& d, int K, const uint8_t* x, uint8_t* out_rev,
                       unsigned long long* out_len, cudaStream_t stream) {
+    PairDev dw = d;
+    const size_t pm_bytes = size_t(d.sigma) * size_t(d.prob[0].W) * 4;
+    dw.walk_pm_smem = pm_bytes <= 200 * 1024 ? 1 : 0;
+    const int smem = dw.walk_pm_smem ? int(pm_bytes) : 0;
+    auto launch = [&](auto kern) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             smem);
+        if (e != cudaSuccess) return e;
+        kern<<<1, 32, smem, stream>>>(dw, x, out_rev, out_len);
+        return cudaGetLastError();
+    };
     switch (K) {
-        case 1: pair_walk_kernel<1><<<1, 32, 0, stream>>>(d, x, out_rev, out_len); break;
-        case 2: pair_walk_kernel<2><<<1, 32, 0, stream>>>(d, x, out_rev, out_len); break;
-        case 4: pair_walk_kernel<4><<<1, 32, 0, stream>>>(d, x, out_rev, out_len); break;
-        case 8: pair_walk_kernel<8><<<1, 32, 0, stream>>>(d, x, out_rev, out_len); break;
+        case 1: return launch(pair_walk_kernel<1>);
+        case 2: return launch(pair_walk_kernel<2>);
+        case 4: return launch(pair_walk_kernel<4>);
+        case 8: return launch(pair_walk_kernel<8>);
         default: return cudaErrorInvalidValue;
     }
-    return cudaGetLastError();
 }
 
 }  // namespace wlcs

@@ -5,6 +5,7 @@
 // dispatches to the kernels.  There is deliberately no CPU compute path: if
 // CUDA is unusable every compute entry point fails with WLCS_E_NO_DEVICE.
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -156,11 +157,11 @@ struct PairPlan {
     int K = 1;
 };
 
-// Words per lane.  Cost model (cycles ~ steps x per-row ALU ops): the fill
-// takes max(total strip-steps / resident warps, critical path) steps, where
-// the critical path is ~40 steps of hand-off skew per strip plus the rows of
-// one strip; a row costs ~3K+3 ALU ops.  Small K = more parallel strips but
-// more per-word overhead and a longer skew chain.
+// Words per lane.  Cost model in cycles, calibrated on B200 (single-strip
+// probe, tools/pair_probe.py): a 16-row step costs kStep[K] cycles when the
+// strip has a sub-partition to itself; strips start ~60 steps apart (lane
+// pipeline + hand-off); strips beyond the resident warps run in waves; more
+// resident strips than sub-partitions share issue slots.
 int choose_k(const Ctx& c, int64_t W, int64_t rows_per_prob, int sigma, int nprob) {
     const int forced = env_int("WLCS_PAIR_K", 0);
     if (forced == 1 || forced == 2 || forced == 4 || forced == 8) return forced;
@@ -168,12 +169,16 @@ int choose_k(const Ctx& c, int64_t W, int64_t rows_per_prob, int sigma, int npro
     double best = 1e300;
     int best_k = 1;
     for (int K : {1, 2, 4, 8}) {
-        if (wlcs::pair_smem_bytes(K, sigma) > 200 * 1024) continue;
+        const int smem = wlcs::pair_smem_bytes(K, sigma);
+        if (smem > 200 * 1024) continue;
+        const double step = K == 1 ? 430 : K == 2 ? 490 : K == 4 ? 680 : 1100;
         const double strips = double((W + 32 * K - 1) / (32 * K));
         const double total = strips * nprob;
-        const double warps = std::min(total, 4.0 * c.sms);
-        const double steps = std::max(total * chunks / warps, strips * 40.0 + chunks);
-        const double cost = steps * (3.0 * K + 3.0);
+        const double per_sm = std::min(32, (227 * 1024) / std::max(smem, 1));
+        const double active = std::min(total, per_sm * c.sms);
+        const double share = std::max(1.0, active / (4.0 * c.sms));
+        const double waves = std::ceil(total / active);
+        const double cost = (waves * chunks + strips * 60.0) * step * share;
         if (cost < best) {
             best = cost;
             best_k = K;
@@ -191,6 +196,7 @@ void set_problem(wlcs::FillProblem& P, int64_t rows, uint32_t* pmg, int64_t cols
     P.nchunks = int((rows + 15) / 16);
     P.Mpad = int64_t(P.nchunks) * 16;
     P.Dpad = P.Mpad + 512;
+    P.cwords = ((int64_t(P.nchunks) + 3) & ~int64_t(3)) + 8;
 }
 
 bool use_split(int64_t rows, bool store) {
@@ -255,12 +261,12 @@ int pair_setup(Ctx& c, const uint8_t* d_row, int64_t rows, const uint8_t* d_col,
     }
     size_t carry_words = 0;
     for (int q = 0; q < d.nprob; ++q)
-        carry_words += size_t(d.prob[q].nstrips) * size_t(d.prob[q].nchunks);
+        carry_words += size_t(d.prob[q].nstrips) * size_t(d.prob[q].cwords);
     WLCS_CUDA(c.carry.ensure(carry_words * 4 + 256));
     uint32_t* carry = c.carry.as<uint32_t>();
     for (int q = 0; q < d.nprob; ++q) {
         d.prob[q].carry = carry;
-        carry += size_t(d.prob[q].nstrips) * size_t(d.prob[q].nchunks);
+        carry += size_t(d.prob[q].nstrips) * size_t(d.prob[q].cwords);
     }
     WLCS_CUDA(cudaMemsetAsync(c.carry.p, 0, carry_words * 4, c.stream));
     WLCS_CUDA(cudaMemsetAsync(d.ticket, 0, 4 + 4 + 8 + 8, c.stream));
@@ -289,7 +295,8 @@ int pair_length_device(Ctx& c, const uint8_t* dx, size_t m, const uint8_t* dy, s
     }
     // Length is symmetric: sweep the shorter string as rows so the
     // sequential dimension is short and the parallel (strip) dimension wide.
-    const bool x_rows = m <= n;
+    const int orient = env_int("WLCS_PAIR_ROWS", 0);  // diagnostics: 1 = x rows, 2 = y rows
+    const bool x_rows = orient == 1 ? true : orient == 2 ? false : m <= n;
     PairPlan plan;
     int rc = x_rows ? pair_setup(c, dx, int64_t(m), dy, int64_t(n), false, plan)
                     : pair_setup(c, dy, int64_t(n), dx, int64_t(m), false, plan);

@@ -53,7 +53,8 @@ struct FillProblem {
     int64_t cols;
     int nstrips;            // ceil(W / (32 K))
     int nchunks;            // 16-row chunks of the row string
-    uint32_t* carry;        // [nstrips][nchunks] carry words, zero-initialised
+    uint32_t* carry;        // [nstrips][cwords] carry words, zero-initialised
+    int64_t cwords;         // carry-row stride: round_up(nchunks, 4) + 8
     uint32_t* v_out;        // optional: final V words [>= W]
     unsigned long long* zeros;  // optional: LCS accumulator
     uint32_t* rows_out;     // optional: bit rows, diagonal layout (traceback)
@@ -66,7 +67,7 @@ struct PairDev {
     FillProblem prob[2];
     int nprob;
     uint32_t code_stride;   // smem bytes per code record (set by pair_fill)
-    int carry_win;          // chunks per carry-word window (set by pair_fill)
+    int walk_pm_smem;       // walk keeps the match-mask table in shared memory
     const uint8_t* colp0;   // column string of problem 0 (alphabet scan)
     const uint16_t* map;    // 256 byte -> code map of the column alphabet
     int sigma;              // codes incl. the zero row
