@@ -66,6 +66,8 @@ def parse_args():
                     help="target CPU work of the bounded reference sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--variant", choices=["bitparallel", "wavefront"], default="bitparallel",
+                    help="fill kernel variant (WLCS_VARIANT_*)")
     return ap.parse_args()
 
 
@@ -277,10 +279,12 @@ def run_c2(args, dist):
     d_out = torch.zeros(args.pairs, dtype=torch.int32, device=dev)
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
 
+    variant = wl.VARIANT_WAVEFRONT if args.variant == "wavefront" else wl.VARIANT_BITPARALLEL
+
     def step():
         wl.lcs_length_batch_device(d_xs.data_ptr(), d_xo.data_ptr(), d_ys.data_ptr(),
                                    d_yo.data_ptr(), args.pairs, xs_bytes, ys_bytes,
-                                   d_out.data_ptr(), stream.cuda_stream)
+                                   d_out.data_ptr(), stream.cuda_stream, variant=variant)
 
     for _ in range(args.warmup):
         flush.zero_()
@@ -320,7 +324,7 @@ def run_c2(args, dist):
 
         def e2e_step():
             wl._check(wl.lib.wlcs_length_batch_ex(xs.ctypes.data, xop, ys.ctypes.data, yop,
-                                                  args.pairs, 0, outp))
+                                                  args.pairs, variant, outp))
         e2e_step()
         dist.barrier()
         wall = []
@@ -341,7 +345,10 @@ def run_c2(args, dist):
     peak = ctypes.c_double()
     wl._check(wl.lib.wlcs_probe_int_peak(5, ctypes.byref(peak)))
     kernel_ms = float(np.mean(main_ms))
-    alg_ops = cells * 3.0 / 32.0
+    wave = variant == wl.VARIANT_WAVEFRONT
+    # algorithmic int ops: bit-parallel 3 per 32-cell word-row; cell wavefront
+    # 3 per cell (match test, max, add-max)
+    alg_ops = cells * 3.0 if wave else cells * 3.0 / 32.0
     achieved = alg_ops / (kernel_ms * 1e-3) / 1e12
     peak_t = peak.value / 1e12
     line = {
@@ -355,14 +362,18 @@ def run_c2(args, dist):
                    "global_batch": args.pairs * dist.world, "seq_len": "200-1000",
                    "parallelism": f"pair-sharded x{dist.world} (no collective)",
                    "cells_per_gpu_step": cells, "l2": "flushed between steps (300 MB write)"},
-        "gpu_launches": 4 * args.steps,  # plan, scan, scatter, main (CUB-free)
+        # bit-parallel: plan, scan, scatter, main (CUB-free); wavefront: one kernel
+        "gpu_launches": (1 if wave else 4) * args.steps,
+        "variant": args.variant,
         "roofline": {"bound": "int", "achieved": round(achieved, 3), "peak": round(peak_t, 3),
-                     "unit": "Tops/s (int32 ALU, 3 ops per 32-cell word-row)",
+                     "unit": "Tops/s (int32 ALU, 3 ops per cell)" if wave else
+                             "Tops/s (int32 ALU, 3 ops per 32-cell word-row)",
                      "frac": round(achieved / peak_t, 4), "traffic": None,
-                     "kernel": "batch_main_kernel", "kernel_ms": round(kernel_ms, 4),
+                     "kernel": "wave_batch_kernel" if wave else "batch_main_kernel",
+                     "kernel_ms": round(kernel_ms, 4),
                      "kernel_share_of_step": round(kernel_ms / (total_ms / args.steps), 3),
                      "peak_source": "measured live: wlcs_probe_int_peak (LOP3 stream)",
-                     "gcups_ceiling": round(peak.value * 32 / 3 / 1e9, 1)},
+                     "gcups_ceiling": round(peak.value * (1 if wave else 32) / 3 / 1e9, 1)},
         "clocks": clocks.summary(),
     }
     if e2e:
@@ -404,8 +415,11 @@ def run_pair_config(args, dist):
             "c4": "C4: 1M x 1M DNA, length only",
             "c5": "C5: 2M x 500k Zipf(1.1) bytes, length only"}[args.config]
     cells = len(x) * len(y)
+    variant = wl.VARIANT_WAVEFRONT if args.variant == "wavefront" else wl.VARIANT_BITPARALLEL
+    if variant == wl.VARIANT_WAVEFRONT:
+        sub = False  # the cell-wavefront variant computes lengths only
     fn = (lambda: wl.lcs_subsequence(x, y, wl.NO_BUDGET)) if sub else \
-        (lambda: wl.lcs_length(x, y, wl.NO_BUDGET))
+        (lambda: wl.lcs_length(x, y, wl.NO_BUDGET, variant=variant))
     for _ in range(args.warmup):
         res = fn()
     times, fill_ms = [], []
@@ -426,7 +440,10 @@ def run_pair_config(args, dist):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t * 1e3, 3),
             "higher_is_better": True, "scaling": "none", "vs_baseline": None, "dtype": "u32",
             "data": "synthetic (paper_1306_4627_b200/workloads.py)",
-            "config": {"workload": name, "lcs_length": length, "m": len(x), "n": len(y)},
+            "config": {"workload": name + ("" if sub or args.config not in ("c1", "c3")
+                                           else " (length only)"),
+                       "lcs_length": length, "m": len(x), "n": len(y)},
+            "variant": args.variant,
             "fill_kernel_ms": round(float(np.mean(fill_ms)), 3),
             "fill_gcups": round(cells / (float(np.mean(fill_ms)) * 1e-3) / 1e9, 1)
             if np.mean(fill_ms) > 0 else None,

@@ -84,7 +84,7 @@ struct Ctx {
     // batch
     DevBuf xs, ys, xoff, yoff, out, ws;
     // single pair
-    DevBuf px, py, pmg, carry, small, rows, outrev, codes, ry, vbuf;
+    DevBuf px, py, pmg, carry, small, rows, outrev, codes, ry, vbuf, wave;
     ~Ctx() {
         if (stream) cudaStreamDestroy(stream);
     }
@@ -323,15 +323,103 @@ int pair_length_device(Ctx& c, const uint8_t* dx, size_t m, const uint8_t* dy, s
     return WLCS_OK;
 }
 
+// Cell-wavefront variant for one pair (wavefront.cu): rows = the longer
+// string (more bands in flight), columns = the shorter one.
+int pair_wave_device(Ctx& c, const uint8_t* dx, size_t m, const uint8_t* dy, size_t n,
+                     uint32_t* out) {
+    if (m == 0 || n == 0) {
+        *out = 0;
+        return WLCS_OK;
+    }
+    const bool x_rows = m >= n;
+    wlcs::WavePairDev d{};
+    d.rowp = x_rows ? dx : dy;
+    d.m = int64_t(x_rows ? m : n);
+    d.colp = x_rows ? dy : dx;
+    d.n = int64_t(x_rows ? n : m);
+    if (d.n >= (int64_t(1) << 24))
+        return fail(WLCS_E_CONFIG, "wavefront variant: the shorter string must be < 2^24 bytes");
+    d.bstride = ((d.n + 64) + 31) & ~int64_t(31);
+    const int64_t bands = wlcs::wave_pair_bands(d.m);
+    const int64_t budget = int64_t(1) << 30;  // boundary-row ring
+    int64_t nbuf = budget / (d.bstride * 4);
+    if (nbuf > bands) nbuf = bands;
+    if (nbuf < 2) nbuf = 2;
+    d.nbuf = uint32_t(nbuf);
+    const size_t bytes = size_t(nbuf) * size_t(d.bstride) * 4;
+    WLCS_CUDA(c.wave.ensure(bytes));
+    WLCS_CUDA(c.small.ensure(4096));
+    d.bnd = c.wave.as<uint32_t>();
+    d.ticket = reinterpret_cast<uint32_t*>(c.small.as<uint8_t>() + 1600);
+    d.out = d.ticket + 1;
+    WLCS_CUDA(cudaMemsetAsync(d.bnd, 0, bytes, c.stream));
+    WLCS_CUDA(cudaMemsetAsync(d.ticket, 0, 8, c.stream));
+    if (c.timing && !c.ev0) {
+        WLCS_CUDA(cudaEventCreate(&c.ev0));
+        WLCS_CUDA(cudaEventCreate(&c.ev1));
+    }
+    if (c.timing) WLCS_CUDA(cudaEventRecord(c.ev0, c.stream));
+    WLCS_CUDA(wlcs::wave_pair_launch(d, c.sms, c.stream));
+    if (c.timing) WLCS_CUDA(cudaEventRecord(c.ev1, c.stream));
+    WLCS_CUDA(cudaMemcpyAsync(out, d.out, 4, cudaMemcpyDeviceToHost, c.stream));
+    WLCS_CUDA(cudaStreamSynchronize(c.stream));
+    if (c.timing) WLCS_CUDA(cudaEventElapsedTime(&c.last_main_ms, c.ev0, c.ev1));
+    return WLCS_OK;
+}
+
+int pair_length_variant(Ctx& c, const uint8_t* dx, size_t m, const uint8_t* dy, size_t n,
+                        int variant, uint32_t* out) {
+    if (variant == WLCS_VARIANT_WAVEFRONT) return pair_wave_device(c, dx, m, dy, n, out);
+    return pair_length_device(c, dx, m, dy, n, out);
+}
+
 // ------------------------------------------------------------------ batch
 int batch_device(Ctx& c, const uint8_t* d_xs, const uint64_t* d_xoff, const uint8_t* d_ys,
                  const uint64_t* d_yoff, size_t pairs, uint64_t xs_bytes, uint64_t ys_bytes,
                  int variant, uint32_t* d_out, cudaStream_t stream) {
     if (pairs == 0) return WLCS_OK;
     if (pairs > 0x7fffffffull) return fail(WLCS_E_INVALID_ARGUMENT, "too many pairs in one batch");
-    if (variant != WLCS_VARIANT_BITPARALLEL)
-        return fail(WLCS_E_CONFIG, "fill variant " + std::to_string(variant) +
-                                       " is not available for batches");
+    if (variant != WLCS_VARIANT_BITPARALLEL && variant != WLCS_VARIANT_WAVEFRONT)
+        return fail(WLCS_E_CONFIG, "unknown fill variant " + std::to_string(variant));
+    if (variant == WLCS_VARIANT_WAVEFRONT) {
+        WLCS_CUDA(c.ws.ensure(8 + size_t(pairs) * 4));
+        wlcs::WaveBatchDev d{};
+        d.xs = d_xs;
+        d.xoff = d_xoff;
+        d.ys = d_ys;
+        d.yoff = d_yoff;
+        d.out = d_out;
+        d.pairs = uint32_t(pairs);
+        d.counter = c.ws.as<uint32_t>();
+        d.overflow_count = d.counter + 1;
+        d.overflow = d.counter + 2;
+        WLCS_CUDA(cudaMemsetAsync(d.counter, 0, 8, stream));
+        if (c.timing && !c.ev0) {
+            WLCS_CUDA(cudaEventCreate(&c.ev0));
+            WLCS_CUDA(cudaEventCreate(&c.ev1));
+        }
+        if (c.timing) WLCS_CUDA(cudaEventRecord(c.ev0, stream));
+        WLCS_CUDA(wlcs::wave_batch_launch(d, c.sms, stream));
+        if (c.timing) WLCS_CUDA(cudaEventRecord(c.ev1, stream));
+        uint32_t overflow = 0;
+        WLCS_CUDA(cudaMemcpyAsync(&overflow, d.overflow_count, 4, cudaMemcpyDeviceToHost, stream));
+        WLCS_CUDA(cudaStreamSynchronize(stream));
+        if (c.timing) WLCS_CUDA(cudaEventElapsedTime(&c.last_main_ms, c.ev0, c.ev1));
+        if (overflow == 0) return WLCS_OK;
+        std::vector<uint32_t> ids(overflow);
+        WLCS_CUDA(cudaMemcpy(ids.data(), d.overflow, overflow * 4, cudaMemcpyDeviceToHost));
+        for (uint32_t p : ids) {
+            uint64_t xo[2], yo[2];
+            WLCS_CUDA(cudaMemcpy(xo, d_xoff + p, 16, cudaMemcpyDeviceToHost));
+            WLCS_CUDA(cudaMemcpy(yo, d_yoff + p, 16, cudaMemcpyDeviceToHost));
+            uint32_t len = 0;
+            int rc = pair_wave_device(c, d_xs + xo[0], size_t(xo[1] - xo[0]), d_ys + yo[0],
+                                      size_t(yo[1] - yo[0]), &len);
+            if (rc) return rc;
+            WLCS_CUDA(cudaMemcpy(d_out + p, &len, 4, cudaMemcpyHostToDevice));
+        }
+        return WLCS_OK;
+    }
     const int pm_bytes = env_int("WLCS_BATCH_PM_KB", 24) * 1024;
     const size_t ws_bytes = wlcs::batch_workspace_bytes(uint32_t(pairs), pm_bytes);
     WLCS_CUDA(c.ws.ensure(ws_bytes));
@@ -413,9 +501,8 @@ int wlcs_length_ex(const uint8_t* x, size_t m, const uint8_t* y, size_t n, size_
     Ctx* c = nullptr;
     rc = get_ctx(&c);
     if (rc) return rc;
-    if (variant != WLCS_VARIANT_BITPARALLEL)
-        return fail(WLCS_E_CONFIG, "fill variant " + std::to_string(variant) +
-                                       " is not available for single pairs");
+    if (variant != WLCS_VARIANT_BITPARALLEL && variant != WLCS_VARIANT_WAVEFRONT)
+        return fail(WLCS_E_CONFIG, "unknown fill variant " + std::to_string(variant));
     if (m == 0 || n == 0) {
         *out = 0;
         return WLCS_OK;
@@ -426,7 +513,7 @@ int wlcs_length_ex(const uint8_t* x, size_t m, const uint8_t* y, size_t n, size_
     WLCS_CUDA(cudaMemcpyAsync(c->py.p, y, n, cudaMemcpyHostToDevice, c->stream));
     const uint8_t* dx = c->px.as<uint8_t>();
     const uint8_t* dy = c->py.as<uint8_t>();
-    return pair_length_device(*c, dx, m, dy, n, out);
+    return pair_length_variant(*c, dx, m, dy, n, variant, out);
 }
 
 int wlcs_length(const uint8_t* x, size_t m, const uint8_t* y, size_t n, size_t memory_budget,
@@ -443,10 +530,9 @@ int wlcs_length_device(const uint8_t* d_x, size_t m, const uint8_t* d_y, size_t 
     Ctx* c = nullptr;
     int rc = get_ctx(&c);
     if (rc) return rc;
-    if (variant != WLCS_VARIANT_BITPARALLEL)
-        return fail(WLCS_E_CONFIG, "fill variant " + std::to_string(variant) +
-                                       " is not available for single pairs");
-    return pair_length_device(*c, d_x, m, d_y, n, out);
+    if (variant != WLCS_VARIANT_BITPARALLEL && variant != WLCS_VARIANT_WAVEFRONT)
+        return fail(WLCS_E_CONFIG, "unknown fill variant " + std::to_string(variant));
+    return pair_length_variant(*c, d_x, m, d_y, n, variant, out);
 }
 
 int wlcs_subsequence(const uint8_t* x, size_t m, const uint8_t* y, size_t n,

@@ -91,3 +91,39 @@ cudaError_t pair_walk(const PairDev& d, int K, const uint8_t* x, uint8_t* out_re
                       unsigned long long* out_len, cudaStream_t stream);
 
 }  // namespace wlcs
+
+namespace wlcs {
+
+// ---- cell-wavefront variant (wavefront.cu) ----
+constexpr int kWaveMaxCols = 4096;  // batch kernel: shorter string per pair
+
+struct WaveBatchDev {
+    const uint8_t* xs;
+    const uint64_t* xoff;
+    const uint8_t* ys;
+    const uint64_t* yoff;
+    uint32_t* out;
+    uint32_t pairs;
+    uint32_t* counter;         // pair ticket (zeroed)
+    uint32_t* overflow_count;  // pairs whose shorter string exceeds kWaveMaxCols
+    uint32_t* overflow;        // their indices
+};
+
+struct WavePairDev {
+    const uint8_t* rowp;  // rows (m bytes)
+    int64_t m;
+    const uint8_t* colp;  // columns (n bytes)
+    int64_t n;
+    uint32_t* bnd;        // [nbuf][bstride] ring of boundary rows (value << 8 | tag), zeroed
+    int64_t bstride;      // >= n + 64
+    uint32_t nbuf;        // >= 2
+    uint32_t* ticket;     // band ticket (zeroed)
+    uint32_t* out;        // LCS length
+};
+
+size_t wave_batch_smem();
+cudaError_t wave_batch_launch(const WaveBatchDev& d, int sms, cudaStream_t stream);
+int64_t wave_pair_bands(int64_t m);
+cudaError_t wave_pair_launch(const WavePairDev& d, int sms, cudaStream_t stream);
+
+}  // namespace wlcs

@@ -215,3 +215,49 @@ def test_cpp_facade_reference_unit_cases():
     r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "PASS" in r.stdout
+
+
+# ---- cell-wavefront (DPX) variant: same integer results as the oracle ----
+
+def check_batch_variant(wl, restatement, xs, ys, variant):
+    xb, xo, yb, yo = wl.pack_pairs(xs, ys)
+    got = wl.lcs_length_batch(xb, xo, yb, yo, variant=variant)
+    want = restatement.length_batch(xb, xo, yb, yo)
+    bad = np.nonzero(got != want)[0]
+    assert bad.size == 0, f"{bad.size} mismatches, first pair {bad[0]}: got {got[bad[0]]} want {want[bad[0]]}"
+
+
+@pytest.mark.parametrize("alphabet", [DNA, PROTEIN])
+def test_wavefront_batch_random(wl, restatement, alphabet):
+    rng = np.random.default_rng(99)
+    xs, ys = rand_pairs(rng, 2000, 0, 400, alphabet)
+    check_batch_variant(wl, restatement, xs, ys, wl.VARIANT_WAVEFRONT)
+
+
+def test_wavefront_batch_edges(wl, restatement):
+    rng = np.random.default_rng(6)
+    a = np.arange(256, dtype=np.uint8)
+    xs = [b"", b"A", b"", b"AAAA", b"A" * 1000, bytes(a), b"AC" * 2100, b"G" * 5000]
+    ys = [b"", b"", b"A", b"AAAA", b"C" * 1000, bytes(a[::-1]), b"CA" * 2100, b"G" * 4500]
+    for _ in range(30):  # 256-symbol alphabet, bands of 128 rows with ragged ends
+        m, n = int(rng.integers(1, 700)), int(rng.integers(1, 700))
+        xs.append(a[rng.integers(0, 256, m)].tobytes())
+        ys.append(a[rng.integers(0, 256, n)].tobytes())
+    check_batch_variant(wl, restatement, xs, ys, wl.VARIANT_WAVEFRONT)
+
+
+@pytest.mark.parametrize("m,n", [(1, 1), (127, 129), (129, 127), (1000, 1000), (4096, 33),
+                                 (5000, 200), (20000, 7000)])
+def test_wavefront_pair(wl, restatement, m, n):
+    rng = np.random.default_rng(m * 7 + n)
+    x = rng.choice(np.frombuffer(DNA, np.uint8), m).tobytes()
+    y = rng.choice(np.frombuffer(DNA, np.uint8), n).tobytes()
+    want = restatement.length_bitpar(x, y)
+    assert wl.lcs_length(x, y, variant=wl.VARIANT_WAVEFRONT) == want
+    assert wl.lcs_length(x, y, variant=wl.VARIANT_BITPARALLEL) == want
+
+
+def test_wavefront_c1_checkpoint(wl):
+    from paper_1306_4627_b200 import workloads
+    x, y = workloads.config_pair("c1")
+    assert wl.lcs_length(x, y, variant=wl.VARIANT_WAVEFRONT) == 6538
