@@ -66,6 +66,8 @@ def parse_args():
                     help="target CPU work of the bounded reference sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--colsplit", action="store_true",
+                    help="c4/c5: use the multi-GPU column-split path even on one GPU")
     ap.add_argument("--variant", choices=["bitparallel", "wavefront"], default="bitparallel",
                     help="fill kernel variant (WLCS_VARIANT_*)")
     return ap.parse_args()
@@ -402,6 +404,75 @@ def cpu_baseline_c2(args, xs, xo, ys, yo, gpu_lengths):
                       f"lengths identical to the GPU's (equivalence gate)"}
 
 
+def run_colsplit(args, dist):
+    """C4/C5 on N GPUs: one long pair, column slice per rank (strong scaling).
+    Carries cross GPUs inside the fill (the producer kernel stores into the
+    consumer's inbox through an IPC peer pointer); the length comes from one
+    all_gather + one MAX all_reduce (multigpu.colsplit_combine_dist)."""
+    import torch
+    import paper_1306_4627_b200 as wl
+    from paper_1306_4627_b200 import multigpu, workloads
+    torch.cuda.set_device(dist.local_rank)
+    dev = torch.device("cuda", dist.local_rank)
+    import torch.distributed as tdist
+    x, y = workloads.config_pair(args.config, args.seed)
+    rows, cols = (x, y) if len(x) <= len(y) else (y, x)
+    G, g = dist.world, dist.rank
+    lo, hi = multigpu.colsplit_bounds(len(cols), G)[g]
+    words = wl.colsplit_inbox_words(len(rows))
+    in_f, in_r = wl.device_alloc(4 * words), wl.device_alloc(4 * words)
+    handles = [(None, None)] * G
+    if G > 1:
+        tdist.all_gather_object(handles, (wl.ipc_handle(in_f), wl.ipc_handle(in_r)))
+    out_f = wl.ipc_open(handles[g + 1][0]) if g + 1 < G else 0
+    out_r = wl.ipc_open(handles[g - 1][1]) if g > 0 else 0
+
+    def step():
+        wl.device_zero(in_f, 4 * words)
+        wl.device_zero(in_r, 4 * words)
+        torch.cuda.synchronize()
+        dist.barrier()
+        vf, vr = wl.colsplit_fill(rows, cols, lo, hi, wl.COLSPLIT_FORWARD | wl.COLSPLIT_REVERSE,
+                                  in_fwd=in_f if g > 0 else 0, out_fwd=out_f,
+                                  in_rev=in_r if g + 1 < G else 0, out_rev=out_r)
+        if G == 1:
+            return multigpu.colsplit_combine([(lo, hi)], [vf], [vr], len(cols))
+        return multigpu.colsplit_combine_dist(lo, hi, vf, vr, tdist, device=dev)
+
+    for _ in range(args.warmup):
+        length = step()
+    wl._check(wl.lib.wlcs_set_timing(1))
+    km = ctypes.c_float()
+    wall, fill = [], []
+    with ClockSampler(dist.local_rank) as clocks:
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            length = step()
+            wall.append(time.perf_counter() - t0)
+            wl._check(wl.lib.wlcs_last_kernel_ms(ctypes.byref(km)))
+            fill.append(km.value)
+    wl._check(wl.lib.wlcs_set_timing(0))
+    fill_ms = dist.max(float(np.mean(fill)))
+    wall_s = dist.max(float(np.mean(wall)))
+    if out_f:
+        wl.ipc_close(out_f)
+    if out_r:
+        wl.ipc_close(out_r)
+    cells = len(x) * len(y)
+    return {"metric": METRIC, "value": round(cells / (fill_ms * 1e-3) / 1e9, 3), "unit": UNIT,
+            "n_gpus": G, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(fill_ms, 3), "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "u32", "data": "synthetic (workloads.py)",
+            "config": {"workload": f"{args.config.upper()} single pair, column split x{G}",
+                       "lcs_length": length, "m": len(x), "n": len(y),
+                       "parallelism": f"column slices x{G}, carries over NVLink P2P (IPC)"},
+            "e2e": {"value": round(cells / wall_s / 1e9, 3), "unit": UNIT,
+                    "h2d_bytes_per_step": len(x) + len(y), "d2h_bytes_per_step": 0},
+            "gpu_launches": None, "clocks": clocks.summary(),
+            "note": "value: device fill time (CUDA events, max over ranks); e2e: wall time "
+                    "incl. inbox reset, barrier, H2D, fill and the distributed combine"}
+
+
 def run_pair_config(args, dist):
     """C1/C3 (length + subsequence) and C4/C5 (length only), single GPU."""
     import torch
@@ -459,6 +530,8 @@ def main():
     dist.init()
     if args.config == "c2":
         line = run_c2(args, dist)
+    elif (dist.world > 1 or args.colsplit) and args.config in ("c4", "c5"):
+        line = run_colsplit(args, dist)
     else:
         line = run_pair_config(args, dist)
     if dist.rank == 0:

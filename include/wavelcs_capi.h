@@ -144,6 +144,52 @@ int wlcs_generate_pairs(size_t pairs, size_t lo, size_t hi, const uint8_t* alpha
                         size_t alphabet_len, uint64_t seed, uint8_t* xs, uint64_t* x_off,
                         uint8_t* ys, uint64_t* y_off);
 
+/* ---- multi-GPU column split of one long pair ----
+ *
+ * The bidirectional bit-parallel fill of (x, y) is cut into column slices,
+ * one per GPU / rank; rank g owns columns [col_lo, col_hi) of y.  Two
+ * problems share the slice: FORWARD = rows x[0, m/2) against y[col_lo,
+ * col_hi); REVERSE = rows x[m/2, m) reversed against the slice reversed.
+ * Between neighbouring slices only one carry word per 16 rows travels (the
+ * strip kernel's hand-off): forward carries flow from rank g-1 to rank g,
+ * reverse carries from rank g+1 to rank g.  The producer's kernel writes them
+ * straight into the consumer's INBOX (device memory of the consumer GPU,
+ * reached through a peer / IPC pointer) as self-validating words; the
+ * consumer's kernel polls its inbox -- the exchange is fused into the fill.
+ *
+ * Inboxes: wlcs_colsplit_inbox_words(m) 32-bit words per problem, allocated
+ * with wlcs_device_alloc (zeroed) and shared across processes with
+ * wlcs_ipc_handle / wlcs_ipc_open.  An inbox must be re-zeroed
+ * (wlcs_device_zero) before every fill that uses it.
+ *
+ * wlcs_colsplit_fill: problems = WLCS_COLSPLIT_FORWARD | WLCS_COLSPLIT_REVERSE
+ * (both in one launch in production; separately when a single device plays
+ * several ranks in order, see tests).  d_in_* = this rank's inboxes (NULL
+ * for the first slice of that direction), d_out_* = the neighbour's inboxes
+ * (NULL for the last slice).  On return v_fwd / v_rev (host arrays of
+ * ceil((col_hi - col_lo) / 32) words, may be NULL for a problem not run)
+ * hold the slice's final bit vectors; the LCS length is then
+ *   max_k F[k] + R[k],  F[k] = zero bits of the forward vectors below column
+ *   k, R[k] = zero bits of the reverse vectors below n - k
+ * (paper_1306_4627_b200/multigpu.py: colsplit_combine). */
+#define WLCS_COLSPLIT_FORWARD 1
+#define WLCS_COLSPLIT_REVERSE 2
+int wlcs_colsplit_inbox_words(size_t m, size_t* words);
+int wlcs_colsplit_fill(const uint8_t* x, size_t m, const uint8_t* y, size_t n, size_t col_lo,
+                       size_t col_hi, int problems, const uint32_t* d_in_fwd,
+                       uint32_t* d_out_fwd, const uint32_t* d_in_rev, uint32_t* d_out_rev,
+                       uint32_t* v_fwd, uint32_t* v_rev);
+
+/* Device memory helpers for the inboxes (current device). */
+int wlcs_device_alloc(size_t bytes, void** d_ptr); /* zero-filled */
+int wlcs_device_zero(void* d_ptr, size_t bytes);
+int wlcs_device_free(void* d_ptr);
+/* cudaIpcMemHandle_t as 64 opaque bytes, for exchanging inboxes between
+ * processes (one process per GPU); peer access is enabled on open. */
+int wlcs_ipc_handle(void* d_ptr, uint8_t handle[64]);
+int wlcs_ipc_open(const uint8_t handle[64], void** d_ptr);
+int wlcs_ipc_close(void* d_ptr);
+
 #ifdef __cplusplus
 }
 #endif

@@ -112,6 +112,15 @@ lib.wlcs_generate_pairs.argtypes = [_sz, _sz, _sz, _vp, _sz, ctypes.c_uint64, _v
 lib.wlcs_set_timing.argtypes = [ctypes.c_int]
 lib.wlcs_last_kernel_ms.argtypes = [ctypes.POINTER(ctypes.c_float)]
 lib.wlcs_probe_int_peak.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_double)]
+lib.wlcs_colsplit_inbox_words.argtypes = [_sz, ctypes.POINTER(ctypes.c_size_t)]
+lib.wlcs_colsplit_fill.argtypes = [_vp, _sz, _vp, _sz, _sz, _sz, ctypes.c_int, _vp, _vp, _vp, _vp,
+                                   _vp, _vp]
+lib.wlcs_device_alloc.argtypes = [_sz, ctypes.POINTER(ctypes.c_void_p)]
+lib.wlcs_device_zero.argtypes = [_vp, _sz]
+lib.wlcs_device_free.argtypes = [_vp]
+lib.wlcs_ipc_handle.argtypes = [_vp, ctypes.c_char_p]
+lib.wlcs_ipc_open.argtypes = [ctypes.c_char_p, ctypes.POINTER(ctypes.c_void_p)]
+lib.wlcs_ipc_close.argtypes = [_vp]
 
 
 def _check(rc: int) -> None:
@@ -203,3 +212,60 @@ def generate_random(length: int, alphabet, seed: int) -> bytes:
     out = ctypes.create_string_buffer(max(1, length))
     _check(lib.wlcs_generate_random(length, a, len(a), seed & (2 ** 64 - 1), out))
     return out.raw[:length]
+
+
+# ---- multi-GPU column split (include/wavelcs_capi.h, wlcs_colsplit_*) ----
+COLSPLIT_FORWARD = 1
+COLSPLIT_REVERSE = 2
+
+
+def colsplit_inbox_words(m: int) -> int:
+    w = ctypes.c_size_t()
+    _check(lib.wlcs_colsplit_inbox_words(m, ctypes.byref(w)))
+    return int(w.value)
+
+
+def device_alloc(nbytes: int) -> int:
+    p = ctypes.c_void_p()
+    _check(lib.wlcs_device_alloc(nbytes, ctypes.byref(p)))
+    return int(p.value)
+
+
+def device_zero(ptr: int, nbytes: int) -> None:
+    _check(lib.wlcs_device_zero(ptr, nbytes))
+
+
+def device_free(ptr: int) -> None:
+    _check(lib.wlcs_device_free(ptr))
+
+
+def ipc_handle(ptr: int) -> bytes:
+    buf = ctypes.create_string_buffer(64)
+    _check(lib.wlcs_ipc_handle(ptr, buf))
+    return buf.raw
+
+
+def ipc_open(handle: bytes) -> int:
+    p = ctypes.c_void_p()
+    _check(lib.wlcs_ipc_open(handle, ctypes.byref(p)))
+    return int(p.value)
+
+
+def ipc_close(ptr: int) -> None:
+    _check(lib.wlcs_ipc_close(ptr))
+
+
+def colsplit_fill(x, y, col_lo: int, col_hi: int, problems: int = 3, in_fwd: int = 0,
+                  out_fwd: int = 0, in_rev: int = 0, out_rev: int = 0):
+    """This rank's slice of the bidirectional fill; returns (v_fwd, v_rev) as
+    uint32 arrays (None for a problem not run)."""
+    xb, yb = _as_bytes(x), _as_bytes(y)
+    words = (col_hi - col_lo + 31) // 32
+    vf = np.zeros(words, np.uint32) if problems & COLSPLIT_FORWARD else None
+    vr = np.zeros(words, np.uint32) if problems & COLSPLIT_REVERSE else None
+    _check(lib.wlcs_colsplit_fill(xb, len(xb), yb, len(yb), col_lo, col_hi, problems,
+                                  in_fwd or None, out_fwd or None, in_rev or None,
+                                  out_rev or None,
+                                  vf.ctypes.data if vf is not None else None,
+                                  vr.ctypes.data if vr is not None else None))
+    return vf, vr

@@ -126,6 +126,24 @@ __device__ __forceinline__ uint4 ld_relaxed_gpu_v4(const uint32_t* p) {
                  : "memory");
     return v;
 }
+// System-scope variants for the carry words that cross GPUs (column split:
+// the producer writes into the consumer's memory over NVLink / P2P).
+__device__ __forceinline__ uint32_t ld_relaxed_sys(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ uint4 ld_relaxed_sys_v4(const uint32_t* p) {
+    uint4 v;
+    asm volatile("ld.relaxed.sys.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p)
+                 : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_relaxed_sys(uint32_t* p, uint32_t v) {
+    asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ void st_relaxed_gpu(uint32_t* p, uint32_t v) {
     asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -214,16 +232,27 @@ __global__ void __launch_bounds__(32 * kPairWarps) pair_strip_kernel(PairDev d) 
         uint32_t V[K];
 #pragma unroll
         for (int k = 0; k < K; ++k) V[k] = 0xffffffffu;
-        const bool has_left = strip > 0;
-        const bool has_right = strip + 1 < uint32_t(P.nstrips);
+        // the slice's first strip takes its carries from ext_in and its last
+        // strip sends them to ext_out when the pair is split across GPUs
+        const bool ext_left = strip == 0 && P.ext_in != nullptr;
+        const bool ext_right = strip + 1 == uint32_t(P.nstrips) && P.ext_out != nullptr;
+        const bool has_left = strip > 0 || ext_left;
+        const bool has_right = strip + 1 < uint32_t(P.nstrips) || ext_right;
         const int64_t cwords = P.cwords;  // carry-row stride (multiple of 4)
-        const uint32_t* left_carry = P.carry + int64_t(has_left ? strip - 1 : 0) * cwords;
-        uint32_t* my_carry = P.carry + int64_t(strip) * cwords;
+        const uint32_t* left_carry =
+            ext_left ? P.ext_in : P.carry + int64_t(strip > 0 ? strip - 1 : 0) * cwords;
+        uint32_t* my_carry = ext_right ? P.ext_out : P.carry + int64_t(strip) * cwords;
         const bool feeder = has_left && lane == 0;
+        auto carry_ld = [&](const uint32_t* q) {
+            return ext_left ? ld_relaxed_sys(q) : ld_relaxed_gpu(q);
+        };
+        auto carry_ld4 = [&](const uint32_t* q) {
+            return ext_left ? ld_relaxed_sys_v4(q) : ld_relaxed_gpu_v4(q);
+        };
         // lane 0 reads the left strip's carry words four chunks at a time, one
         // group ahead (words past nchunks are never written and stay 0)
         uint4 cw = make_uint4(0, 0, 0, 0), cw_next = cw;
-        if (feeder) cw_next = ld_relaxed_gpu_v4(left_carry);
+        if (feeder) cw_next = carry_ld4(left_carry);
         StoreHook<K, STORE> hook{
             STORE ? P.rows_out + ((int64_t(strip) * P.Dpad) * 32 + lane) * K : nullptr, 0};
         const int T = (nchunks + 31 + 3) & ~3;
@@ -250,8 +279,8 @@ __global__ void __launch_bounds__(32 * kPairWarps) pair_strip_kernel(PairDev d) 
                 uint32_t* w = &cw.x;
 #pragma unroll
                 for (int j = 0; j < 4; ++j)
-                    while (tg + j < nchunks && w[j] == 0u) w[j] = ld_relaxed_gpu(left_carry + tg + j);
-                cw_next = ld_relaxed_gpu_v4(left_carry + tg + 4);
+                    while (tg + j < nchunks && w[j] == 0u) w[j] = carry_ld(left_carry + tg + j);
+                cw_next = carry_ld4(left_carry + tg + 4);
             }
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
@@ -286,8 +315,11 @@ __global__ void __launch_bounds__(32 * kPairWarps) pair_strip_kernel(PairDev d) 
                     hook(r, valid, V);
                 }
                 const uint32_t nh = __shfl_up_sync(kFullMask, cout_hi, 1);
-                if (has_right && lane == 31 && valid)
-                    st_relaxed_gpu(my_carry + ch, kCarryValid | (cout_lo << 8) | cout_hi);
+                if (has_right && lane == 31 && valid) {
+                    const uint32_t word = kCarryValid | (cout_lo << 8) | cout_hi;
+                    if (ext_right) st_relaxed_sys(my_carry + ch, word);
+                    else st_relaxed_gpu(my_carry + ch, word);
+                }
                 cin_lo = nl << 24;
                 cin_hi = nh << 24;
                 r0 = r1;

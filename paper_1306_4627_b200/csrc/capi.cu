@@ -81,11 +81,15 @@ struct Ctx {
     float last_main_ms = -1.f;
     int sms = 148;
     cudaStream_t stream = nullptr;
+    cudaStream_t copy_stream = nullptr;  // host batch pipeline: H2D of chunk k+1 || compute of k
+    std::vector<cudaEvent_t> chunk_ev;
     // batch
     DevBuf xs, ys, xoff, yoff, out, ws;
     // single pair
     DevBuf px, py, pmg, carry, small, rows, outrev, codes, ry, vbuf, wave;
     ~Ctx() {
+        for (cudaEvent_t e : chunk_ev) cudaEventDestroy(e);
+        if (copy_stream) cudaStreamDestroy(copy_stream);
         if (stream) cudaStreamDestroy(stream);
     }
 };
@@ -463,6 +467,87 @@ int batch_device(Ctx& c, const uint8_t* d_xs, const uint64_t* d_xoff, const uint
     return WLCS_OK;
 }
 
+// Host batch with the host->device copies pipelined against the compute:
+// the pairs are cut into nchunks contiguous chunks; chunk k's string bytes are
+// copied on copy_stream while chunk k-1 runs on the compute stream (its own
+// workspace, so the chunks' plans never overlap).  Overflow pairs (too long
+// or too large an alphabet for one warp) are finished afterwards.
+int batch_host_pipelined(Ctx& c, const uint8_t* xs, const uint64_t* x_off, const uint8_t* ys,
+                         const uint64_t* y_off, size_t pairs, int nchunks, uint32_t* out) {
+    const uint64_t xs_bytes = x_off[pairs], ys_bytes = y_off[pairs];
+    if (!c.copy_stream) WLCS_CUDA(cudaStreamCreateWithFlags(&c.copy_stream, cudaStreamNonBlocking));
+    while (int(c.chunk_ev.size()) < nchunks) {
+        cudaEvent_t e;
+        WLCS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        c.chunk_ev.push_back(e);
+    }
+    const int pm_bytes = env_int("WLCS_BATCH_PM_KB", 24) * 1024;
+    std::vector<size_t> p0(nchunks + 1);
+    for (int k = 0; k <= nchunks; ++k) p0[k] = pairs * size_t(k) / size_t(nchunks);
+    std::vector<size_t> ws_off(nchunks + 1, 0);
+    for (int k = 0; k < nchunks; ++k)
+        ws_off[k + 1] = ws_off[k] + ((wlcs::batch_workspace_bytes(uint32_t(p0[k + 1] - p0[k]),
+                                                                  pm_bytes) + 255) & ~size_t(255));
+    WLCS_CUDA(c.ws.ensure(ws_off[nchunks]));
+    cudaStream_t cs = c.copy_stream, s = c.stream;
+    uint8_t* dxs = c.xs.as<uint8_t>();
+    uint8_t* dys = c.ys.as<uint8_t>();
+    WLCS_CUDA(cudaMemcpyAsync(c.xoff.p, x_off, (pairs + 1) * 8, cudaMemcpyHostToDevice, cs));
+    WLCS_CUDA(cudaMemcpyAsync(c.yoff.p, y_off, (pairs + 1) * 8, cudaMemcpyHostToDevice, cs));
+    if (c.timing && !c.ev0) {
+        WLCS_CUDA(cudaEventCreate(&c.ev0));
+        WLCS_CUDA(cudaEventCreate(&c.ev1));
+    }
+    for (int k = 0; k < nchunks; ++k) {
+        const uint64_t xa = x_off[p0[k]], xb = x_off[p0[k + 1]];
+        const uint64_t ya = y_off[p0[k]], yb = y_off[p0[k + 1]];
+        if (xb > xa) WLCS_CUDA(cudaMemcpyAsync(dxs + xa, xs + xa, xb - xa, cudaMemcpyHostToDevice, cs));
+        if (yb > ya) WLCS_CUDA(cudaMemcpyAsync(dys + ya, ys + ya, yb - ya, cudaMemcpyHostToDevice, cs));
+        WLCS_CUDA(cudaEventRecord(c.chunk_ev[k], cs));
+        WLCS_CUDA(cudaStreamWaitEvent(s, c.chunk_ev[k], 0));
+        wlcs::BatchDev d{};
+        d.xs = dxs;
+        d.xoff = c.xoff.as<uint64_t>() + p0[k];
+        d.xs_bytes = xs_bytes;
+        d.ys = dys;
+        d.yoff = c.yoff.as<uint64_t>() + p0[k];
+        d.ys_bytes = ys_bytes;
+        d.out = c.out.as<uint32_t>() + p0[k];
+        d.pairs = uint32_t(p0[k + 1] - p0[k]);
+        d.pm_bytes = pm_bytes;
+        const bool ends = k == 0 || k == nchunks - 1;
+        WLCS_CUDA(wlcs::batch_launch(d, c.ws.as<uint8_t>() + ws_off[k], c.sms, s,
+                                     (c.timing && ends && k == 0) ? c.ev0 : nullptr,
+                                     (c.timing && ends && k == nchunks - 1) ? c.ev1 : nullptr));
+    }
+    WLCS_CUDA(cudaMemcpyAsync(out, c.out.p, pairs * 4, cudaMemcpyDeviceToHost, s));
+    std::vector<uint32_t> ovf(nchunks, 0);
+    for (int k = 0; k < nchunks; ++k)
+        WLCS_CUDA(cudaMemcpyAsync(&ovf[k],
+                                  wlcs::batch_overflow_count_ptr(c.ws.as<uint8_t>() + ws_off[k],
+                                                                 uint32_t(p0[k + 1] - p0[k])),
+                                  4, cudaMemcpyDeviceToHost, s));
+    WLCS_CUDA(cudaStreamSynchronize(s));
+    if (c.timing) WLCS_CUDA(cudaEventElapsedTime(&c.last_main_ms, c.ev0, c.ev1));
+    for (int k = 0; k < nchunks; ++k) {
+        if (!ovf[k]) continue;
+        std::vector<uint32_t> ids(ovf[k]);
+        WLCS_CUDA(cudaMemcpy(ids.data(),
+                             wlcs::batch_overflow_list_ptr(c.ws.as<uint8_t>() + ws_off[k],
+                                                           uint32_t(p0[k + 1] - p0[k])),
+                             ovf[k] * 4, cudaMemcpyDeviceToHost));
+        for (uint32_t q : ids) {
+            const size_t p = p0[k] + q;
+            uint32_t len = 0;
+            int rc = pair_length_device(c, dxs + x_off[p], size_t(x_off[p + 1] - x_off[p]),
+                                        dys + y_off[p], size_t(y_off[p + 1] - y_off[p]), &len);
+            if (rc) return rc;
+            out[p] = len;
+        }
+    }
+    return WLCS_OK;
+}
+
 int validate_offsets(const uint64_t* off, size_t pairs, const char* name) {
     for (size_t k = 0; k < pairs; ++k)
         if (off[k + 1] < off[k])
@@ -618,6 +703,11 @@ int wlcs_length_batch_ex(const uint8_t* xs, const uint64_t* x_off, const uint8_t
     WLCS_CUDA(c->yoff.ensure((pairs + 1) * 8));
     WLCS_CUDA(c->out.ensure(pairs * 4));
     cudaStream_t s = c->stream;
+    const int nchunks = variant == WLCS_VARIANT_BITPARALLEL
+                            ? int(std::min<size_t>(8, pairs / 8192))
+                            : 1;
+    if (nchunks >= 2 && xs_bytes + ys_bytes >= (16u << 20))
+        return batch_host_pipelined(*c, xs, x_off, ys, y_off, pairs, nchunks, out);
     if (xs_bytes) WLCS_CUDA(cudaMemcpyAsync(c->xs.p, xs, xs_bytes, cudaMemcpyHostToDevice, s));
     if (ys_bytes) WLCS_CUDA(cudaMemcpyAsync(c->ys.p, ys, ys_bytes, cudaMemcpyHostToDevice, s));
     WLCS_CUDA(cudaMemcpyAsync(c->xoff.p, x_off, (pairs + 1) * 8, cudaMemcpyHostToDevice, s));
@@ -705,6 +795,160 @@ int wlcs_generate_random(size_t length, const uint8_t* alphabet, size_t alphabet
         return fail(WLCS_E_INVALID_ARGUMENT, "generate_random: alphabet must not be empty");
     std::mt19937_64 rng(seed);
     for (size_t k = 0; k < length; ++k) out[k] = alphabet[rng() % alphabet_len];
+    return WLCS_OK;
+}
+
+// ------------------------------------------------------- column split
+int wlcs_colsplit_inbox_words(size_t m, size_t* words) {
+    if (!words) return fail(WLCS_E_INVALID_ARGUMENT, "words is NULL");
+    const size_t rows = m - m / 2;  // the larger half
+    const size_t nch = (rows + 15) / 16;
+    *words = ((nch + 3) & ~size_t(3)) + 8;
+    return WLCS_OK;
+}
+
+int wlcs_colsplit_fill(const uint8_t* x, size_t m, const uint8_t* y, size_t n, size_t col_lo,
+                       size_t col_hi, int problems, const uint32_t* d_in_fwd,
+                       uint32_t* d_out_fwd, const uint32_t* d_in_rev, uint32_t* d_out_rev,
+                       uint32_t* v_fwd, uint32_t* v_rev) {
+    if (!x || !y) return fail(WLCS_E_INVALID_ARGUMENT, "NULL input");
+    if (m < 2) return fail(WLCS_E_INVALID_ARGUMENT, "column split needs at least 2 rows");
+    if (!(col_lo < col_hi && col_hi <= n))
+        return fail(WLCS_E_INVALID_ARGUMENT, "column slice out of range");
+    if (problems < 1 || problems > 3) return fail(WLCS_E_INVALID_ARGUMENT, "bad problems mask");
+    Ctx* c = nullptr;
+    int rc = get_ctx(&c);
+    if (rc) return rc;
+    const int64_t cols = int64_t(col_hi - col_lo);
+    const int64_t W = (cols + 31) / 32;
+    WLCS_CUDA(c->px.ensure(m + 16));
+    WLCS_CUDA(c->py.ensure(size_t(cols) + 16));
+    WLCS_CUDA(cudaMemcpyAsync(c->px.p, x, m, cudaMemcpyHostToDevice, c->stream));
+    WLCS_CUDA(cudaMemcpyAsync(c->py.p, y + col_lo, size_t(cols), cudaMemcpyHostToDevice,
+                              c->stream));
+    const uint8_t* dx = c->px.as<uint8_t>();
+    const uint8_t* dcol = c->py.as<uint8_t>();
+    wlcs::PairDev d{};
+    d.colp0 = dcol;
+    d.prob[0].cols = cols;
+    WLCS_CUDA(c->small.ensure(4096));
+    uint8_t* sb = c->small.as<uint8_t>();
+    uint16_t* map = reinterpret_cast<uint16_t*>(sb + 1024);
+    d.ticket = reinterpret_cast<uint32_t*>(sb + 1540);
+    d.safe16 = reinterpret_cast<const uint4*>(sb + 2048);
+    int sigma = 0;
+    WLCS_CUDA(wlcs::pair_prepare(d, reinterpret_cast<uint32_t*>(sb), map,
+                                 reinterpret_cast<uint32_t*>(sb + 1536), c->stream, &sigma));
+    const int64_t mid = int64_t(m / 2);
+    const bool want[2] = {(problems & WLCS_COLSPLIT_FORWARD) != 0,
+                          (problems & WLCS_COLSPLIT_REVERSE) != 0};
+    d.nprob = (want[0] ? 1 : 0) + (want[1] ? 1 : 0);
+    const int K = choose_k(*c, W, int64_t(m) - mid, sigma, d.nprob);
+    if (wlcs::pair_smem_bytes(K, sigma) > 220 * 1024)
+        return fail(WLCS_E_INTERNAL, "match-mask table does not fit in shared memory");
+    const size_t pm_words = size_t(sigma) * size_t(W);
+    WLCS_CUDA(c->pmg.ensure(pm_words * 4 * 2));
+    WLCS_CUDA(c->vbuf.ensure(size_t(W) * 8 + 64));
+    WLCS_CUDA(c->ry.ensure(size_t(cols) + 16));
+    uint32_t* pmg = c->pmg.as<uint32_t>();
+    int q = 0;
+    size_t code_vecs = 0;
+    int which[2];
+    for (int dir = 0; dir < 2; ++dir) {
+        if (!want[dir]) continue;
+        wlcs::FillProblem& P = d.prob[q];
+        set_problem(P, dir == 0 ? mid : int64_t(m) - mid, pmg + pm_words * dir, cols, K);
+        P.v_out = c->vbuf.as<uint32_t>() + W * dir;
+        P.ext_in = dir == 0 ? d_in_fwd : d_in_rev;
+        P.ext_out = dir == 0 ? d_out_fwd : d_out_rev;
+        code_vecs += 4 * size_t(wlcs::pair_code_plane(P.nchunks));
+        which[q++] = dir;
+    }
+    WLCS_CUDA(c->codes.ensure(code_vecs * 16));
+    uint4* code_base = c->codes.as<uint4>();
+    size_t carry_words = 0;
+    for (int k = 0; k < d.nprob; ++k) {
+        wlcs::FillProblem& P = d.prob[k];
+        const bool rev = which[k] == 1;
+        WLCS_CUDA(wlcs::pair_code_rows(rev ? dx + mid : dx, P.rows, rev, map, K, P, code_base,
+                                       c->stream));
+        code_base += 4 * wlcs::pair_code_plane(P.nchunks);
+        carry_words += size_t(P.nstrips) * size_t(P.cwords);
+    }
+    WLCS_CUDA(c->carry.ensure(carry_words * 4 + 256));
+    uint32_t* carry = c->carry.as<uint32_t>();
+    for (int k = 0; k < d.nprob; ++k) {
+        d.prob[k].carry = carry;
+        carry += size_t(d.prob[k].nstrips) * size_t(d.prob[k].cwords);
+    }
+    WLCS_CUDA(cudaMemsetAsync(c->carry.p, 0, carry_words * 4, c->stream));
+    WLCS_CUDA(cudaMemsetAsync(d.ticket, 0, 4, c->stream));
+    WLCS_CUDA(cudaMemsetAsync(sb + 2048, 0, 16, c->stream));
+    if (want[0]) WLCS_CUDA(wlcs::pair_build_pm(dcol, cols, map, sigma, W, pmg, c->stream));
+    if (want[1]) {
+        WLCS_CUDA(wlcs::pair_reverse(dcol, cols, c->ry.as<uint8_t>(), c->stream));
+        WLCS_CUDA(wlcs::pair_build_pm(c->ry.as<uint8_t>(), cols, map, sigma, W, pmg + pm_words,
+                                      c->stream));
+    }
+    // both problems have the same strip count (same columns)
+    if (c->timing && !c->ev0) {
+        WLCS_CUDA(cudaEventCreate(&c->ev0));
+        WLCS_CUDA(cudaEventCreate(&c->ev1));
+    }
+    if (c->timing) WLCS_CUDA(cudaEventRecord(c->ev0, c->stream));
+    WLCS_CUDA(wlcs::pair_fill(d, K, false, c->sms, c->stream));
+    if (c->timing) WLCS_CUDA(cudaEventRecord(c->ev1, c->stream));
+    if (want[0] && v_fwd)
+        WLCS_CUDA(cudaMemcpyAsync(v_fwd, c->vbuf.as<uint32_t>(), size_t(W) * 4,
+                                  cudaMemcpyDeviceToHost, c->stream));
+    if (want[1] && v_rev)
+        WLCS_CUDA(cudaMemcpyAsync(v_rev, c->vbuf.as<uint32_t>() + W, size_t(W) * 4,
+                                  cudaMemcpyDeviceToHost, c->stream));
+    WLCS_CUDA(cudaStreamSynchronize(c->stream));
+    if (c->timing) WLCS_CUDA(cudaEventElapsedTime(&c->last_main_ms, c->ev0, c->ev1));
+    return WLCS_OK;
+}
+
+int wlcs_device_alloc(size_t bytes, void** d_ptr) {
+    if (!d_ptr) return fail(WLCS_E_INVALID_ARGUMENT, "d_ptr is NULL");
+    Ctx* c = nullptr;
+    int rc = get_ctx(&c);
+    if (rc) return rc;
+    WLCS_CUDA(cudaMalloc(d_ptr, bytes ? bytes : 16));
+    WLCS_CUDA(cudaMemset(*d_ptr, 0, bytes ? bytes : 16));
+    return WLCS_OK;
+}
+
+int wlcs_device_zero(void* d_ptr, size_t bytes) {
+    if (!d_ptr) return fail(WLCS_E_INVALID_ARGUMENT, "d_ptr is NULL");
+    WLCS_CUDA(cudaMemset(d_ptr, 0, bytes));
+    return WLCS_OK;
+}
+
+int wlcs_device_free(void* d_ptr) {
+    if (d_ptr) WLCS_CUDA(cudaFree(d_ptr));
+    return WLCS_OK;
+}
+
+int wlcs_ipc_handle(void* d_ptr, uint8_t handle[64]) {
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+    if (!d_ptr || !handle) return fail(WLCS_E_INVALID_ARGUMENT, "NULL argument");
+    cudaIpcMemHandle_t h;
+    WLCS_CUDA(cudaIpcGetMemHandle(&h, d_ptr));
+    std::memcpy(handle, &h, 64);
+    return WLCS_OK;
+}
+
+int wlcs_ipc_open(const uint8_t handle[64], void** d_ptr) {
+    if (!d_ptr || !handle) return fail(WLCS_E_INVALID_ARGUMENT, "NULL argument");
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, 64);
+    WLCS_CUDA(cudaIpcOpenMemHandle(d_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    return WLCS_OK;
+}
+
+int wlcs_ipc_close(void* d_ptr) {
+    if (d_ptr) WLCS_CUDA(cudaIpcCloseMemHandle(d_ptr));
     return WLCS_OK;
 }
 

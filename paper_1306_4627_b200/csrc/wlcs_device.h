@@ -60,6 +60,11 @@ struct FillProblem {
     uint32_t* rows_out;     // optional: bit rows, diagonal layout (traceback)
     int64_t Mpad;           // nchunks * 16
     int64_t Dpad;           // diagonals per strip in rows_out = Mpad + 512
+    // column split across GPUs: carries of the slice's first strip come from
+    // ext_in (written by the neighbour GPU), the last strip's go to ext_out
+    // (the neighbour's inbox, a peer pointer); both [cwords] words, zeroed
+    const uint32_t* ext_in;
+    uint32_t* ext_out;
 };
 
 // One strip-kernel launch: 1 or 2 problems sharing the column alphabet.

@@ -261,3 +261,46 @@ def test_wavefront_c1_checkpoint(wl):
     from paper_1306_4627_b200 import workloads
     x, y = workloads.config_pair("c1")
     assert wl.lcs_length(x, y, variant=wl.VARIANT_WAVEFRONT) == 6538
+
+
+# ---- multi-GPU column split, played in order on ONE device ----
+# (a slice's fill only runs once its inbox is complete, so no kernel waits on
+# another; the carries still travel through the inbox words exactly as they do
+# between GPUs)
+
+def _colsplit_in_order(wl, x, y, world):
+    from paper_1306_4627_b200 import multigpu
+    bounds = multigpu.colsplit_bounds(len(y), world)
+    words = wl.colsplit_inbox_words(len(x))
+    inbox_f = [wl.device_alloc(4 * words) for _ in range(world)]
+    inbox_r = [wl.device_alloc(4 * words) for _ in range(world)]
+    vf, vr = [None] * world, [None] * world
+    try:
+        for g in range(world):  # forward: slice g reads inbox_f[g], writes inbox_f[g+1]
+            lo, hi = bounds[g]
+            vf[g], _ = wl.colsplit_fill(x, y, lo, hi, wl.COLSPLIT_FORWARD,
+                                        in_fwd=inbox_f[g] if g > 0 else 0,
+                                        out_fwd=inbox_f[g + 1] if g + 1 < world else 0)
+        for g in reversed(range(world)):  # reverse: right to left
+            lo, hi = bounds[g]
+            _, vr[g] = wl.colsplit_fill(x, y, lo, hi, wl.COLSPLIT_REVERSE,
+                                        in_rev=inbox_r[g] if g + 1 < world else 0,
+                                        out_rev=inbox_r[g - 1] if g > 0 else 0)
+    finally:
+        for p in inbox_f + inbox_r:
+            wl.device_free(p)
+    return multigpu.colsplit_combine(bounds, vf, vr, len(y))
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 4])
+def test_colsplit_in_order(wl, restatement, world):
+    rng = np.random.default_rng(world)
+    x = rng.choice(np.frombuffer(DNA, np.uint8), 20011).tobytes()
+    y = rng.choice(np.frombuffer(DNA, np.uint8), 30007).tobytes()
+    assert _colsplit_in_order(wl, x, y, world) == restatement.length_bitpar(x, y)
+
+
+def test_colsplit_c1(wl):
+    from paper_1306_4627_b200 import workloads
+    x, y = workloads.config_pair("c1")
+    assert _colsplit_in_order(wl, x, y, 2) == 6538

@@ -91,7 +91,56 @@ def _strip_worker(rank, port, out):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("worker", [_batch_worker, _strip_worker])
+def _colsplit_worker(rank, port, out):
+    """Bidirectional column split (the C4 multi-GPU decomposition): forward
+    carries flow rank 0 -> 1, reverse carries rank 1 -> 0, the length comes
+    from colsplit_combine_dist (all_gather of zero totals + MAX all_reduce)."""
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import torch
+    import oracle
+    from paper_1306_4627_b200 import multigpu
+    _init(rank, port)
+    res = oracle.Restatement()
+    x = res.generate_random(4001, b"ACGT", 21)
+    y = res.generate_random(2999, b"ACGT", 22)
+    n = len(y)
+    lo, hi = multigpu.colsplit_bounds(n, WORLD)[rank]
+    mid = len(x) // 2
+    words = max(1, (hi - lo + 63) // 64)
+    vf = np.full(words, 2**64 - 1, np.uint64)
+    vr = np.full(words, 2**64 - 1, np.uint64)
+    top = x[:mid]
+    bot = x[mid:][::-1]
+    ycol, ycol_rev = y[lo:hi], y[lo:hi][::-1]
+    # forward: left to right
+    for r0, r1 in multigpu.band_ranges(len(top), 500):
+        cin = None
+        if rank > 0:
+            buf = torch.zeros((r1 - r0 + 7) // 8, dtype=torch.uint8)
+            dist.recv(buf, src=rank - 1)
+            cin = multigpu.unpack_carries(buf.numpy(), r1 - r0)
+        cout = res.strip_rows(top[r0:r1], ycol, vf, cin)
+        if rank < WORLD - 1:
+            dist.send(torch.from_numpy(multigpu.pack_carries(cout).copy()), dst=rank + 1)
+    # reverse: right to left
+    for r0, r1 in multigpu.band_ranges(len(bot), 500):
+        cin = None
+        if rank < WORLD - 1:
+            buf = torch.zeros((r1 - r0 + 7) // 8, dtype=torch.uint8)
+            dist.recv(buf, src=rank + 1)
+            cin = multigpu.unpack_carries(buf.numpy(), r1 - r0)
+        cout = res.strip_rows(bot[r0:r1], ycol_rev, vr, cin)
+        if rank > 0:
+            dist.send(torch.from_numpy(multigpu.pack_carries(cout).copy()), dst=rank - 1)
+    got = multigpu.colsplit_combine_dist(lo, hi, vf, vr, dist)
+    if rank == 0:
+        out["ok"] = got == res.length_bitpar(x, y)
+        out["got"] = got
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("worker", [_batch_worker, _strip_worker, _colsplit_worker])
 def test_two_process_gloo(worker):
     mgr = mp.Manager()
     out = mgr.dict()
@@ -112,3 +161,31 @@ def test_shard_and_strip_planning():
     assert multigpu.band_ranges(10, 4) == [(0, 4), (4, 8), (8, 10)]
     bits = np.random.default_rng(0).integers(0, 2, 77).astype(np.uint8)
     assert np.array_equal(multigpu.unpack_carries(multigpu.pack_carries(bits), 77), bits)
+
+
+def test_colsplit_combine_single_process():
+    """colsplit_combine over oracle slices equals the whole-pair length for
+    1..4 slices and odd widths."""
+    import oracle
+    from paper_1306_4627_b200 import multigpu
+    res = oracle.Restatement()
+    x = res.generate_random(1501, b"ACGT", 5)
+    y = res.generate_random(1234, b"ACGT", 6)
+    want = res.length_bitpar(x, y)
+    mid = len(x) // 2
+    for world in (1, 2, 3, 4):
+        bounds = multigpu.colsplit_bounds(len(y), world)
+        vfs = [None] * world
+        vrs = [None] * world
+        cin = None
+        for g, (lo, hi) in enumerate(bounds):
+            v = np.full(max(1, (hi - lo + 63) // 64), 2**64 - 1, np.uint64)
+            cin = res.strip_rows(x[:mid], y[lo:hi], v, cin)
+            vfs[g] = v
+        cin = None
+        for g in reversed(range(world)):
+            lo, hi = bounds[g]
+            v = np.full(max(1, (hi - lo + 63) // 64), 2**64 - 1, np.uint64)
+            cin = res.strip_rows(x[mid:][::-1], y[lo:hi][::-1], v, cin)
+            vrs[g] = v
+        assert multigpu.colsplit_combine(bounds, vfs, vrs, len(y)) == want, world

@@ -1,1 +1,1 @@
-python -m pytest tests -m gpu -q 2>&1 | tail -3
+timeout 300 python bench.py --config c4 --colsplit --steps 2 --warmup 1 2>&1 | tail -3
