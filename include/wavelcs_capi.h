@@ -180,6 +180,20 @@ int wlcs_colsplit_fill(const uint8_t* x, size_t m, const uint8_t* y, size_t n, s
                        uint32_t* d_out_fwd, const uint32_t* d_in_rev, uint32_t* d_out_rev,
                        uint32_t* v_fwd, uint32_t* v_rev);
 
+/* Single-process multi-GPU conveniences, devices 0..n_gpus-1
+ * of the calling process, one host thread per device:
+ *  - wlcs_length_batch_multi: pairs sharded into contiguous ranges balanced by
+ *    cells (no exchange during compute);
+ *  - wlcs_length_strips: one pair, column split across the devices with the
+ *    carries written straight into the neighbour's inbox over peer access
+ *    (the same fused hand-off as wlcs_colsplit_fill), then the F+R combine.
+ * n_gpus <= 1 runs the single-device path; n_gpus above the visible device
+ * count is WLCS_E_CONFIG. */
+int wlcs_length_batch_multi(const uint8_t* xs, const uint64_t* x_off, const uint8_t* ys,
+                            const uint64_t* y_off, size_t pairs, int n_gpus, uint32_t* out);
+int wlcs_length_strips(const uint8_t* x, size_t m, const uint8_t* y, size_t n, int n_gpus,
+                       uint32_t* out);
+
 /* Device memory helpers for the inboxes (current device). */
 int wlcs_device_alloc(size_t bytes, void** d_ptr); /* zero-filled */
 int wlcs_device_zero(void* d_ptr, size_t bytes);

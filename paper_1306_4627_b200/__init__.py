@@ -121,6 +121,10 @@ lib.wlcs_device_free.argtypes = [_vp]
 lib.wlcs_ipc_handle.argtypes = [_vp, ctypes.c_char_p]
 lib.wlcs_ipc_open.argtypes = [ctypes.c_char_p, ctypes.POINTER(ctypes.c_void_p)]
 lib.wlcs_ipc_close.argtypes = [_vp]
+lib.wlcs_length_batch_multi.argtypes = [_vp, _u64p, _vp, _u64p, _sz, ctypes.c_int,
+                                        ctypes.POINTER(ctypes.c_uint32)]
+lib.wlcs_length_strips.argtypes = [_vp, _sz, _vp, _sz, ctypes.c_int,
+                                   ctypes.POINTER(ctypes.c_uint32)]
 
 
 def _check(rc: int) -> None:
@@ -269,3 +273,27 @@ def colsplit_fill(x, y, col_lo: int, col_hi: int, problems: int = 3, in_fwd: int
                                   vf.ctypes.data if vf is not None else None,
                                   vr.ctypes.data if vr is not None else None))
     return vf, vr
+
+
+def lcs_length_batch_multi(xs, x_off, ys, y_off, n_gpus: int) -> np.ndarray:
+    """Batch sharded over devices 0..n_gpus-1 of this process."""
+    xs = np.ascontiguousarray(np.frombuffer(xs, np.uint8) if isinstance(xs, (bytes, bytearray))
+                              else xs, np.uint8)
+    ys = np.ascontiguousarray(np.frombuffer(ys, np.uint8) if isinstance(ys, (bytes, bytearray))
+                              else ys, np.uint8)
+    x_off = np.ascontiguousarray(x_off, np.uint64)
+    y_off = np.ascontiguousarray(y_off, np.uint64)
+    pairs = len(x_off) - 1
+    out = np.zeros(max(pairs, 0), np.uint32)
+    _check(lib.wlcs_length_batch_multi(xs.ctypes.data, x_off.ctypes.data_as(_u64p), ys.ctypes.data,
+                                       y_off.ctypes.data_as(_u64p), pairs, n_gpus,
+                                       out.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32))))
+    return out
+
+
+def lcs_length_strips(x, y, n_gpus: int) -> int:
+    """One pair, column split over devices 0..n_gpus-1 of this process."""
+    xb, yb = _as_bytes(x), _as_bytes(y)
+    out = ctypes.c_uint32()
+    _check(lib.wlcs_length_strips(xb, len(xb), yb, len(yb), n_gpus, ctypes.byref(out)))
+    return int(out.value)

@@ -11,6 +11,7 @@
 #include <cstring>
 #include <random>
 #include <string>
+#include <thread>
 #include <unordered_map>
 #include <vector>
 
@@ -949,6 +950,147 @@ int wlcs_ipc_open(const uint8_t handle[64], void** d_ptr) {
 
 int wlcs_ipc_close(void* d_ptr) {
     if (d_ptr) WLCS_CUDA(cudaIpcCloseMemHandle(d_ptr));
+    return WLCS_OK;
+}
+
+// ------------------------------------------- single-process multi-GPU
+int wlcs_length_batch_multi(const uint8_t* xs, const uint64_t* x_off, const uint8_t* ys,
+                            const uint64_t* y_off, size_t pairs, int n_gpus, uint32_t* out) {
+    if (n_gpus <= 1) return wlcs_length_batch(xs, x_off, ys, y_off, pairs, out);
+    if (!x_off || !y_off || !out) return fail(WLCS_E_INVALID_ARGUMENT, "NULL argument");
+    if (n_gpus > wlcs_device_count())
+        return fail(WLCS_E_CONFIG, "n_gpus = " + std::to_string(n_gpus) + " but only " +
+                                       std::to_string(wlcs_device_count()) + " devices visible");
+    int rc = validate_offsets(x_off, pairs, "x");
+    if (rc) return rc;
+    rc = validate_offsets(y_off, pairs, "y");
+    if (rc) return rc;
+    // contiguous ranges balanced by cells (paper_1306_4627_b200/multigpu.py: shard_pairs)
+    std::vector<double> cum(pairs + 1, 0.0);
+    for (size_t k = 0; k < pairs; ++k)
+        cum[k + 1] = cum[k] + double(x_off[k + 1] - x_off[k]) * double(y_off[k + 1] - y_off[k]) + 1.0;
+    std::vector<size_t> cut(n_gpus + 1, 0);
+    for (int g = 1; g < n_gpus; ++g)
+        cut[g] = size_t(std::lower_bound(cum.begin(), cum.end(), cum[pairs] * g / n_gpus) -
+                        cum.begin());
+    cut[n_gpus] = pairs;
+    std::vector<int> rcs(n_gpus, WLCS_OK);
+    std::vector<std::string> errs(n_gpus);
+    std::vector<std::thread> th;
+    for (int g = 0; g < n_gpus; ++g) {
+        th.emplace_back([&, g] {
+            const size_t p0 = std::min(cut[g], pairs), p1 = std::max(std::min(cut[g + 1], pairs), p0);
+            if (p1 == p0) return;
+            if (cudaSetDevice(g) != cudaSuccess) {
+                rcs[g] = WLCS_E_CUDA;
+                errs[g] = "cudaSetDevice failed";
+                return;
+            }
+            std::vector<uint64_t> xo(p1 - p0 + 1), yo(p1 - p0 + 1);
+            for (size_t k = p0; k <= p1; ++k) {
+                xo[k - p0] = x_off[k] - x_off[p0];
+                yo[k - p0] = y_off[k] - y_off[p0];
+            }
+            rcs[g] = wlcs_length_batch(xs + x_off[p0], xo.data(), ys + y_off[p0], yo.data(),
+                                       p1 - p0, out + p0);
+            if (rcs[g]) errs[g] = t_err;
+        });
+    }
+    for (auto& t : th) t.join();
+    for (int g = 0; g < n_gpus; ++g)
+        if (rcs[g]) return fail(rcs[g], "device " + std::to_string(g) + ": " + errs[g]);
+    return WLCS_OK;
+}
+
+int wlcs_length_strips(const uint8_t* x, size_t m, const uint8_t* y, size_t n, int n_gpus,
+                       uint32_t* out) {
+    if (!out) return fail(WLCS_E_INVALID_ARGUMENT, "out is NULL");
+    if (n_gpus <= 1 || m < 2 || n < size_t(32 * n_gpus))
+        return wlcs_length(x, m, y, n, WLCS_NO_BUDGET, out);
+    if (n_gpus > wlcs_device_count())
+        return fail(WLCS_E_CONFIG, "n_gpus = " + std::to_string(n_gpus) + " but only " +
+                                       std::to_string(wlcs_device_count()) + " devices visible");
+    // rows = the shorter string, the column string is split
+    const bool x_rows = m <= n;
+    const uint8_t* rows = x_rows ? x : y;
+    const uint8_t* cols = x_rows ? y : x;
+    const size_t M = x_rows ? m : n, N = x_rows ? n : m;
+    const int G = n_gpus;
+    std::vector<size_t> lo(G), hi(G);
+    const size_t words = (N + 31) / 32;
+    for (int g = 0; g < G; ++g) {
+        lo[g] = std::min(N, words * g / G * 32);
+        hi[g] = std::min(N, words * (g + 1) / G * 32);
+    }
+    size_t inbox_words = 0;
+    int rc = wlcs_colsplit_inbox_words(M, &inbox_words);
+    if (rc) return rc;
+    std::vector<void*> in_f(G, nullptr), in_r(G, nullptr);
+    auto cleanup = [&] {
+        for (int g = 0; g < G; ++g) {
+            cudaSetDevice(g);
+            if (in_f[g]) cudaFree(in_f[g]);
+            if (in_r[g]) cudaFree(in_r[g]);
+        }
+    };
+    for (int g = 0; g < G; ++g) {
+        WLCS_CUDA(cudaSetDevice(g));
+        for (int h : {g - 1, g + 1}) {
+            if (h < 0 || h >= G) continue;
+            cudaError_t e = cudaDeviceEnablePeerAccess(h, 0);
+            if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) {
+                cleanup();
+                return cuda_fail(e, "cudaDeviceEnablePeerAccess");
+            }
+            cudaGetLastError();
+        }
+        rc = wlcs_device_alloc(inbox_words * 4, &in_f[g]);
+        if (!rc) rc = wlcs_device_alloc(inbox_words * 4, &in_r[g]);
+        if (rc) {
+            cleanup();
+            return rc;
+        }
+    }
+    std::vector<std::vector<uint32_t>> vf(G), vr(G);
+    std::vector<int> rcs(G, WLCS_OK);
+    std::vector<std::string> errs(G);
+    std::vector<std::thread> th;
+    for (int g = 0; g < G; ++g) {
+        vf[g].assign((hi[g] - lo[g] + 31) / 32, 0u);
+        vr[g].assign((hi[g] - lo[g] + 31) / 32, 0u);
+        th.emplace_back([&, g] {
+            if (cudaSetDevice(g) != cudaSuccess) {
+                rcs[g] = WLCS_E_CUDA;
+                errs[g] = "cudaSetDevice failed";
+                return;
+            }
+            rcs[g] = wlcs_colsplit_fill(
+                rows, M, cols, N, lo[g], hi[g], WLCS_COLSPLIT_FORWARD | WLCS_COLSPLIT_REVERSE,
+                g > 0 ? static_cast<const uint32_t*>(in_f[g]) : nullptr,
+                g + 1 < G ? static_cast<uint32_t*>(in_f[g + 1]) : nullptr,
+                g + 1 < G ? static_cast<const uint32_t*>(in_r[g]) : nullptr,
+                g > 0 ? static_cast<uint32_t*>(in_r[g - 1]) : nullptr, vf[g].data(),
+                vr[g].data());
+            if (rcs[g]) errs[g] = t_err;
+        });
+    }
+    for (auto& t : th) t.join();
+    cleanup();
+    for (int g = 0; g < G; ++g)
+        if (rcs[g]) return fail(rcs[g], "device " + std::to_string(g) + ": " + errs[g]);
+    // combine: L = max_k F[k] + R[k] (multigpu.py: colsplit_combine)
+    std::vector<int64_t> F(N + 1, 0), R(N + 1, 0);
+    size_t k = 0;
+    for (int g = 0; g < G; ++g)
+        for (size_t c = 0; c < hi[g] - lo[g]; ++c, ++k)
+            F[k + 1] = F[k] + (((vf[g][c >> 5] >> (c & 31)) & 1u) ? 0 : 1);
+    k = 0;
+    for (int g = G - 1; g >= 0; --g)
+        for (size_t c = 0; c < hi[g] - lo[g]; ++c, ++k)
+            R[k + 1] = R[k] + (((vr[g][c >> 5] >> (c & 31)) & 1u) ? 0 : 1);
+    int64_t best = 0;
+    for (size_t kk = 0; kk <= N; ++kk) best = std::max(best, F[kk] + R[N - kk]);
+    *out = uint32_t(best);
     return WLCS_OK;
 }
 

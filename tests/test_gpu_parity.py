@@ -304,3 +304,18 @@ def test_colsplit_c1(wl):
     from paper_1306_4627_b200 import workloads
     x, y = workloads.config_pair("c1")
     assert _colsplit_in_order(wl, x, y, 2) == 6538
+
+
+def test_single_process_multi_gpu_entry_points(wl, restatement):
+    rng = np.random.default_rng(3)
+    xs, ys = rand_pairs(rng, 500, 0, 300, PROTEIN)
+    xb, xo, yb, yo = wl.pack_pairs(xs, ys)
+    want = restatement.length_batch(xb, xo, yb, yo)
+    assert np.array_equal(wl.lcs_length_batch_multi(xb, xo, yb, yo, 1), want)
+    x, y = xs[7] * 20, ys[9] * 30
+    assert wl.lcs_length_strips(x, y, 1) == restatement.length_bitpar(x, y)
+    n = wl.device_count()
+    with pytest.raises(wl.ConfigError):
+        wl.lcs_length_batch_multi(xb, xo, yb, yo, n + 1)
+    with pytest.raises(wl.ConfigError):
+        wl.lcs_length_strips(b"ACGT" * 5000, b"GATTACA" * 5000, n + 1)
