@@ -289,7 +289,7 @@ __device__ __forceinline__ uint32_t build_task(const BatchDev& d, const LanePair
                                             uint8_t* smem, uint32_t* zrep) {
     const uint32_t lane = lane_id();
     uint8_t* map = smem;         // byte -> code
-    uint8_t* inv = smem + 256;   // code -> byte
+    uint8_t* inv = smem + 256;   // u16 low-nibble presence per high nibble
     uint8_t* pm = smem + kMapBytes;
     const bool wide = K > 4;
     const uint32_t cs = wide ? 1024u : 128u * uint32_t(K == 3 ? 4 : K);
@@ -337,8 +337,10 @@ __device__ __forceinline__ uint32_t build_task(const BatchDev& d, const LanePair
     }
     __syncwarp();
 
-    // dense codes 1..sigma-1 in byte order (0 = no match), inverse list, zrep
-    uint32_t sigma;
+    // dense codes 1..sigma-1 in byte order (0 = no match), low-nibble
+    // presence per high nibble (in the inv region), zrep
+    uint32_t sigma, hm = 0;
+    uint32_t* hmask = &hm;
     {
         const uint4 f0 = reinterpret_cast<const uint4*>(flags)[lane * 2];
         const uint4 f1 = reinterpret_cast<const uint4*>(flags)[lane * 2 + 1];
@@ -361,10 +363,13 @@ __device__ __forceinline__ uint32_t build_task(const BatchDev& d, const LanePair
             if ((present >> b) & 1u) {
                 if (b < 4) ox |= code << (8 * b);
                 else oy |= code << (8 * (b - 4));
-                inv[code] = uint8_t(8 * lane + uint32_t(b));
                 ++code;
             }
         }
+        // low-nibble presence per high nibble h (lanes 2h, 2h+1 hold bytes 16h..16h+15)
+        const uint32_t upper = __shfl_down_sync(kFullMask, present, 1);
+        const uint32_t nib16 = present | (upper << 8);
+        *hmask = __ballot_sync(kFullMask, (lane & 1u) == 0u && nib16 != 0u);
         const uint32_t absent = ~present & 0xffu;  // exists: at most 255 bytes present
         const uint32_t has = __ballot_sync(kFullMask, absent != 0u);
         const uint32_t zb =
@@ -372,6 +377,7 @@ __device__ __forceinline__ uint32_t build_task(const BatchDev& d, const LanePair
         *zrep = zb * 0x01010101u;
         __syncwarp();
         reinterpret_cast<uint2*>(map)[lane] = make_uint2(ox, oy);
+        if ((lane & 1u) == 0u) reinterpret_cast<uint16_t*>(inv)[lane >> 1] = uint16_t(nib16);
     }
     __syncwarp();
 
@@ -391,20 +397,33 @@ __device__ __forceinline__ uint32_t build_task(const BatchDev& d, const LanePair
             const uint32_t woff =
                 lane_off + (wide ? uint32_t((k >> 2) * 512 + (k & 3) * 4) : uint32_t(k * 4));
             *reinterpret_cast<uint32_t*>(pm + woff) = 0u;  // code 0: the zero row
-            uint32_t hi_acc = 0u, hi_v = 0xffffffffu;
-#pragma unroll 1
-            for (uint32_t c = 1; c < sigma; ++c) {
-                const uint32_t v = inv[c];
-                if ((v >> 4) != hi_v) {  // warp-uniform: codes are sorted by byte value
-                    hi_v = v >> 4;
-                    hi_acc = ~((P[4] ^ (0u - ((v >> 4) & 1u))) | (P[5] ^ (0u - ((v >> 5) & 1u))) |
-                               (P[6] ^ (0u - ((v >> 6) & 1u))) | (P[7] ^ (0u - ((v >> 7) & 1u)))) &
-                             vmask;
+            // match mask of byte v = h*16 + 4j + i:
+            //   hi(h) & b[j] & a[i],  a[i] / b[j] = equality masks of the bit
+            //   pairs (planes 0,1) / (planes 2,3), hi(h) = planes 4..7 == h
+            const uint32_t a[4] = {~(P[0] | P[1]), P[0] & ~P[1], ~P[0] & P[1], P[0] & P[1]};
+            const uint32_t b[4] = {~(P[2] | P[3]), P[2] & ~P[3], ~P[2] & P[3], P[2] & P[3]};
+            uint32_t groups = hm;
+            while (groups) {  // warp-uniform
+                const uint32_t h = uint32_t(__ffs(groups) - 1) >> 1;
+                groups &= groups - 1u;
+                const uint32_t hi_acc =
+                    vmask & ~((P[4] ^ (0u - (h & 1u))) | (P[5] ^ (0u - ((h >> 1) & 1u))) |
+                              (P[6] ^ (0u - ((h >> 2) & 1u))) | (P[7] ^ (0u - ((h >> 3) & 1u))));
+                const uint32_t nm = reinterpret_cast<const uint16_t*>(inv)[h];
+                const uint8_t* mrow = map + h * 16u;
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj) {
+                    if ((nm >> (4 * jj)) & 0xfu) {
+                        const uint32_t hb = hi_acc & b[jj];
+#pragma unroll
+                        for (int ii = 0; ii < 4; ++ii) {
+                            if ((nm >> (4 * jj + ii)) & 1u) {
+                                const uint32_t c = mrow[4 * jj + ii];
+                                *reinterpret_cast<uint32_t*>(pm + c * cs + woff) = hb & a[ii];
+                            }
+                        }
+                    }
                 }
-                const uint32_t m =
-                    hi_acc & ~((P[0] ^ (0u - (v & 1u))) | (P[1] ^ (0u - ((v >> 1) & 1u))) |
-                               (P[2] ^ (0u - ((v >> 2) & 1u))) | (P[3] ^ (0u - ((v >> 3) & 1u))));
-                *reinterpret_cast<uint32_t*>(pm + c * cs + woff) = m;
             }
             c0v = c2v;
             c1v = n1;
