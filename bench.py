@@ -370,7 +370,10 @@ def run_c2(args, dist):
         "roofline": {"bound": "int", "achieved": round(achieved, 3), "peak": round(peak_t, 3),
                      "unit": "Tops/s (int32 ALU, 3 ops per cell)" if wave else
                              "Tops/s (int32 ALU, 3 ops per 32-cell word-row)",
-                     "frac": round(achieved / peak_t, 4), "traffic": None,
+                     "frac": round(achieved / peak_t, 4), "traffic": ncu_traffic(
+                         "wave_batch_kernel" if wave else "batch_main_kernel"),
+                     "algorithmic_bytes": int(xs_bytes + ys_bytes + 16 * (args.pairs + 1)
+                                              + 4 * args.pairs),
                      "kernel": "wave_batch_kernel" if wave else "batch_main_kernel",
                      "kernel_ms": round(kernel_ms, 4),
                      "kernel_share_of_step": round(kernel_ms / (total_ms / args.steps), 3),
@@ -383,6 +386,17 @@ def run_c2(args, dist):
     if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline_c2(args, xs, xo, ys, yo, gpu_lengths)
     return line
+
+
+def ncu_traffic(kernel):
+    """DRAM bytes per launch of `kernel` from the committed ncu capture
+    (profiles/ncu_traffic.json), or None."""
+    try:
+        with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
+                               "ncu_traffic.json")) as f:
+            return json.load(f)[kernel]["dram_bytes_per_launch"]
+    except (OSError, KeyError, ValueError):
+        return None
 
 
 def cpu_baseline_c2(args, xs, xo, ys, yo, gpu_lengths):
