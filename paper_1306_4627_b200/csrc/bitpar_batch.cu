@@ -75,13 +75,14 @@ __global__ void __launch_bounds__(256) batch_plan_kernel(BatchDev d, uint32_t* h
             d.out[p] = 0;  // empty input: length 0 (proj/tests/test_parallel.cpp:236-242)
         } else {
             const uint64_t w = (cols + 31) / 32;
-            if (w > uint64_t(32 * kMaxK) || rows > (uint64_t(1) << 30)) {
+            const uint64_t kmax = uint64_t(d.kmax);
+            if (w > 32 * kmax || rows > (uint64_t(1) << 30)) {
                 // Wider than one warp can hold: routed to the single-pair strip kernel.
                 const uint32_t i = atomicAdd(d.meta + kMetaOverflow, 1u);
                 d.overflow[i] = p;
             } else {
                 int sidx = 0;
-                while ((uint64_t(kMaxK) << sidx) < w) ++sidx;
+                while ((kmax << sidx) < w) ++sidx;
                 const int s = 1 << sidx;
                 const int k = int((w + s - 1) / s);
                 const int order = kNumClasses - 1 - class_of(sidx, k);
@@ -511,10 +512,11 @@ __global__ void __launch_bounds__(32) batch_main_kernel(BatchDev d) {
             WLCS_SWEEP_CASE(0, 1) WLCS_SWEEP_CASE(0, 2) WLCS_SWEEP_CASE(0, 3)
             WLCS_SWEEP_CASE(0, 4) WLCS_SWEEP_CASE(0, 5) WLCS_SWEEP_CASE(0, 6)
             WLCS_SWEEP_CASE(0, 7) WLCS_SWEEP_CASE(0, 8)
-            WLCS_SWEEP_CASE(1, 5) WLCS_SWEEP_CASE(1, 6) WLCS_SWEEP_CASE(1, 7)
-            WLCS_SWEEP_CASE(1, 8)
+            WLCS_SWEEP_CASE(1, 1) WLCS_SWEEP_CASE(1, 2) WLCS_SWEEP_CASE(1, 3)
+            WLCS_SWEEP_CASE(1, 4) WLCS_SWEEP_CASE(1, 5) WLCS_SWEEP_CASE(1, 6)
+            WLCS_SWEEP_CASE(1, 7) WLCS_SWEEP_CASE(1, 8)
             default:
-                break;  // unreachable: S >= 2 always has K >= 5
+                break;  // unreachable
         }
         for (int o = S >> 1; o >= 1; o >>= 1) zeros += __shfl_xor_sync(kFullMask, zeros, o);
         if (active && s == 0) d.out[pair] = uint32_t(zeros);

@@ -144,12 +144,35 @@ __device__ __forceinline__ uint4 ld_relaxed_sys_v4(const uint32_t* p) {
 __device__ __forceinline__ void st_relaxed_sys(uint32_t* p, uint32_t v) {
     asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+// L2-only (cache-global) vector load for polling self-validating words: a
+// weak load that always goes to L2, re-issued because the asm is volatile;
+// no ordering against the thread's own earlier stores is required here.
+__device__ __forceinline__ uint4 ld_cg_v4(const uint32_t* p) {
+    uint4 v;
+    asm volatile("ld.global.cg.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p));
+    return v;
+}
+
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
+// Stores without a "memory" clobber (self-validating words: the compiler may
+// move other accesses across them).
+__device__ __forceinline__ void st_relaxed_gpu_nb(uint32_t* p, uint32_t v) {
+    asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v));
+}
+__device__ __forceinline__ void st_relaxed_sys_nb(uint32_t* p, uint32_t v) {
+    asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v));
+}
 __device__ __forceinline__ void st_relaxed_gpu(uint32_t* p, uint32_t v) {
     asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
 constexpr uint32_t kCarryValid = 0x10000u;  // carry words: valid flag | 16-row mask
-constexpr int kPairWarps = 4;               // max warps per CTA
+constexpr int kPairWarps = 1;               // warps per CTA (one strip per warp; more only shares sub-partitions)
 
 // Row coding: entry i = map[row byte i] (the row's match-mask record in the
 // strip's shared-memory table is at code * code_stride).  Rows
@@ -160,8 +183,9 @@ constexpr int kPairWarps = 4;               // max warps per CTA
 // 4j..4j+3 of every chunk, chunk ch at index ch + kPadChunks, so the warp's
 // j-th LDG.128 (lanes on chunks t-0 .. t-31) is one contiguous 512-byte run.
 // With `reverse` the row string is coded back to front.
-constexpr int kPadChunks = 40;  // >= 31 (lane skew) + 3 (group rounding) + kCodeAhead
-constexpr int kCodeAhead = 4;   // code prefetch distance in steps
+constexpr int kPadChunks = 56;  // >= 31 (lane skew) + 3 (group rounding) + kCodeAhead + kCodeL2Ahead
+constexpr int kCodeAhead = 4;   // code prefetch distance in steps (registers)
+constexpr int kCodeL2Ahead = 12;  // L2 prefetch distance in steps beyond the register ring
 
 struct Codes {
     uint4 a, b, c, d;  // rows 0-3, 4-7, 8-11, 12-15 of a chunk
@@ -194,20 +218,22 @@ __global__ void pair_code_rows_kernel(const uint8_t* row, int64_t rows, int reve
 // Carry handoff between strips: lane 31 of strip s publishes the 16-row carry
 // mask of chunk ch as one relaxed 32-bit store (kCarryValid | mask) into a
 // zero-initialised buffer -- the data word is its own ready flag, so no fence
-// is needed.  Lane 0 of strip s+1 reads the words four chunks at a time (one
-// 16-byte relaxed load), one group of four steps ahead; a word that was still
-// 0 when loaded is re-polled.  Inside the warp the carry masks move with two
+// is needed.  Strip s+1 reads the words four chunks at a time (one 16-byte
+// relaxed load, the same address for the whole warp: a broadcast, so the
+// hand-off code is warp-uniform), two groups of four steps ahead; a group
+// with a word still 0 when loaded is re-polled.  Inside the warp the carry masks move with two
 // shuffles per step (rows 0-7 after row 7, rows 8-15 after row 15), so the
 // shuffle latency hides behind row work.
 //
-// Launch: 1-warp CTAs by default (WLCS_PAIR_WPC selects up to kPairWarps).
+// Launch: 1-warp CTAs (one strip each), up to the occupancy limit.
 template <int K, bool STORE>
-__global__ void __launch_bounds__(32 * kPairWarps) pair_strip_kernel(PairDev d) {
+__global__ void __launch_bounds__(32, 1) pair_strip_kernel(PairDev d) {
     extern __shared__ __align__(16) uint8_t smem[];
-    uint8_t* pm = smem + (threadIdx.x >> 5) * uint32_t(d.sigma) * PmLayout<K>::code_stride;
+    uint8_t* pm = smem;
     constexpr uint32_t cs = PmLayout<K>::code_stride;
     const uint32_t lane = lane_id();
     const uint32_t lane_off = PmLayout<K>::word_offset(lane, 0);
+    uint32_t* sink = d.sink + (int64_t(blockIdx.x) * blockDim.x + threadIdx.x);
     for (;;) {
         uint32_t tk = 0;
         if (lane == 0) tk = atomicAdd(d.ticket, 1u);
@@ -242,31 +268,52 @@ __global__ void __launch_bounds__(32 * kPairWarps) pair_strip_kernel(PairDev d) 
         const uint32_t* left_carry =
             ext_left ? P.ext_in : P.carry + int64_t(strip > 0 ? strip - 1 : 0) * cwords;
         uint32_t* my_carry = ext_right ? P.ext_out : P.carry + int64_t(strip) * cwords;
-        const bool feeder = has_left && lane == 0;
+        // the whole warp loads the (same) carry words -- a broadcast, so the
+        // hand-off code is warp-uniform (no divergence); lane 0 consumes them
+        const bool feeder = has_left;
         auto carry_ld = [&](const uint32_t* q) {
             return ext_left ? ld_relaxed_sys(q) : ld_relaxed_gpu(q);
         };
         auto carry_ld4 = [&](const uint32_t* q) {
-            return ext_left ? ld_relaxed_sys_v4(q) : ld_relaxed_gpu_v4(q);
+            return ext_left ? ld_relaxed_sys_v4(q) : ld_cg_v4(q);
         };
-        // lane 0 reads the left strip's carry words four chunks at a time, one
-        // group ahead (words past nchunks are never written and stay 0)
-        uint4 cw = make_uint4(0, 0, 0, 0), cw_next = cw;
-        if (feeder) cw_next = carry_ld4(left_carry);
         StoreHook<K, STORE> hook{
             STORE ? P.rows_out + ((int64_t(strip) * P.Dpad) * 32 + lane) * K : nullptr, 0};
         const int T = (nchunks + 31 + 3) & ~3;
-        // lane l works on chunk t - l (chunks < 0 / >= nchunks are padding);
-        // codes are prefetched kCodeAhead steps ahead: lane 0's chunk is always
-        // new data (an L2 round trip), the other lanes re-read lane l-1's chunk
+        // lane l works on chunk t - l (chunks < 0 / >= nchunks are padding).
+        // Register rings, no rotation moves (a move of a register with a load
+        // in flight would stall on it): codes of step t live in ring slot
+        // t % 4 and are reloaded, 4 steps ahead, right after their rows; the
+        // left strip's carry words (4 chunks per 16-byte relaxed load) are
+        // loaded one group of 4 steps ahead.
+        // Lane 0's chunk is always new data (an L2 round trip), the other
+        // lanes re-read what lane l-1 read a step earlier.
         const int64_t cstride = P.cstride;
         const uint4* cp = P.coded - int64_t(lane) * cstride;
         auto load_codes = [&](const uint4* q) {
             return Codes{__ldg(q), __ldg(q + plane), __ldg(q + 2 * plane), __ldg(q + 3 * plane)};
         };
-        Codes r0 = load_codes(cp), r1 = load_codes(cp + cstride),
-              r2 = load_codes(cp + 2 * cstride), r3 = load_codes(cp + 3 * cstride);
+        Codes ring[kCodeAhead];
+#pragma unroll
+        for (int j = 0; j < kCodeAhead; ++j) ring[j] = load_codes(cp + j * cstride);
         cp += kCodeAhead * cstride;
+        // carry words travel global -> shared memory by cp.async two groups of
+        // 4 steps ahead (no register waits on a load in flight); ring of 4
+        // 16-byte slots per warp after the match masks
+        uint4 cw = make_uint4(0, 0, 0, 0);
+        uint4* cring = reinterpret_cast<uint4*>(smem + d.pm_warp_bytes);
+        const uint32_t cring_s = uint32_t(__cvta_generic_to_shared(cring));
+        auto carry_async = [&](int g) {  // group g's words -> slot g % 4 (lane 0)
+            if (lane == 0)
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                                 cring_s + uint32_t(g & 3) * 16u),
+                             "l"(left_carry + 4 * g));
+            asm volatile("cp.async.commit_group;");
+        };
+        if (feeder) {
+            carry_async(0);
+            carry_async(1);
+        }
         const uint8_t* pml = pm + lane_off;
         const uint32_t csr = d.code_stride;  // runtime value: address IMAD stays on the FMA pipe
         // carry-in masks of the current step, rows 0-7 / 8-15 at bits 31..24
@@ -275,33 +322,40 @@ __global__ void __launch_bounds__(32 * kPairWarps) pair_strip_kernel(PairDev d) 
         uint32_t cin_lo = 0, cin_hi = 0;
         for (int tg = 0; tg < T; tg += 4) {
             if (feeder && tg < nchunks) {
-                cw = cw_next;
-                uint32_t* w = &cw.x;
-#pragma unroll
-                for (int j = 0; j < 4; ++j)
-                    while (tg + j < nchunks && w[j] == 0u) w[j] = carry_ld(left_carry + tg + j);
-                cw_next = carry_ld4(left_carry + tg + 4);
+                asm volatile("cp.async.wait_group 1;" ::: "memory");  // group tg/4 landed
+                __syncwarp();
+                cw = cring[(tg >> 2) & 3];
+                const int lim = nchunks - tg;  // words at or past nchunks stay 0
+                while ((cw.x == 0u) | (lim > 1 && cw.y == 0u) | (lim > 2 && cw.z == 0u) |
+                       (lim > 3 && cw.w == 0u)) {
+                    cw = carry_ld4(left_carry + tg);  // not yet published: re-poll
+                }
+                __syncwarp();
+                carry_async((tg >> 2) + 2);
+                prefetch_l2(left_carry + tg + 16);
             }
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 const int t = tg + j;
                 const int ch = t - int(lane);
-                const Codes nx = load_codes(cp);
-                cp += cstride;
                 if (lane == 0) {
                     uint32_t fl = j == 0 ? cw.x : j == 1 ? cw.y : j == 2 ? cw.z : cw.w;
                     if (t >= nchunks) fl = 0;  // padding rows take no carry
                     cin_lo = (fl & 0xff00u) << 16;
                     cin_hi = (fl & 0xffu) << 24;
                 }
-                const uint32_t code[16] = {r0.a.x, r0.a.y, r0.a.z, r0.a.w, r0.b.x, r0.b.y,
-                                           r0.b.z, r0.b.w, r0.c.x, r0.c.y, r0.c.z, r0.c.w,
-                                           r0.d.x, r0.d.y, r0.d.z, r0.d.w};
+                Codes& rc = ring[j];
+                const uint32_t code[16] = {rc.a.x, rc.a.y, rc.a.z, rc.a.w, rc.b.x, rc.b.y,
+                                           rc.b.z, rc.b.w, rc.c.x, rc.c.y, rc.c.z, rc.c.w,
+                                           rc.d.x, rc.d.y, rc.d.z, rc.d.w};
                 if constexpr (STORE) hook.dlo = int64_t(t) * 16;
                 const bool valid = ch >= 0 && ch < nchunks;
                 uint32_t Pm[16][K];
 #pragma unroll
                 for (int r = 0; r < 16; ++r) load_pm<K>(pml, code[r] * csr, Pm[r]);
+                rc = load_codes(cp);  // step t + 4
+                prefetch_l2(cp + kCodeL2Ahead * cstride);  // lane 0's chunk: first touch
+                cp += cstride;
                 uint32_t cout_lo = 0, cout_hi = 0;
 #pragma unroll
                 for (int r = 0; r < 8; ++r) {
@@ -315,19 +369,22 @@ __global__ void __launch_bounds__(32 * kPairWarps) pair_strip_kernel(PairDev d) 
                     hook(r, valid, V);
                 }
                 const uint32_t nh = __shfl_up_sync(kFullMask, cout_hi, 1);
-                if (has_right && lane == 31 && valid) {
+                {
+                    // every lane stores (no divergent branch): lane 31's word
+                    // goes to the carry row when it is real, everything else
+                    // to the CTA's sink
+                    const bool pub = has_right && lane == 31 && valid;
+                    uint32_t* dst = pub ? my_carry + ch : sink;
                     const uint32_t word = kCarryValid | (cout_lo << 8) | cout_hi;
-                    if (ext_right) st_relaxed_sys(my_carry + ch, word);
-                    else st_relaxed_gpu(my_carry + ch, word);
+                    if (ext_right) st_relaxed_sys_nb(dst, word);  // warp-uniform branch
+                    else st_relaxed_gpu_nb(dst, word);
                 }
                 cin_lo = nl << 24;
                 cin_hi = nh << 24;
-                r0 = r1;
-                r1 = r2;
-                r2 = r3;
-                r3 = nx;
             }
         }
+        if (feeder) asm volatile("cp.async.wait_all;" ::: "memory");  // ring reused next strip
+        __syncwarp();
         if (P.v_out) {
 #pragma unroll
             for (int k = 0; k < K; ++k)
@@ -652,7 +709,7 @@ cudaError_t pair_split_combine(const uint32_t* vf, const uint32_t* vr, int64_t W
 
 int pair_code_stride(int K) { return K > 4 ? 1024 : 128 * (K == 3 ? 4 : K); }
 
-int pair_smem_bytes(int K, int sigma) { return sigma * pair_code_stride(K); }  // per warp
+int pair_smem_bytes(int K, int sigma) { return sigma * pair_code_stride(K) + 64; }  // per warp
 
 int64_t pair_code_plane(int nchunks) { return int64_t(nchunks) + 2 * kPadChunks; }
 
@@ -679,6 +736,7 @@ cudaError_t pair_code_rows(const uint8_t* row, int64_t rows, bool reverse, const
 template <int K, bool STORE>
 static cudaError_t launch_strip(const PairDev& d, int sms, cudaStream_t stream) {
     const_cast<PairDev&>(d).code_stride = uint32_t(pair_code_stride(K));
+    const_cast<PairDev&>(d).pm_warp_bytes = uint32_t(d.sigma * pair_code_stride(K));
     const char* env = std::getenv("WLCS_PAIR_WPC");
     int wpc = env && *env ? std::atoi(env) : 1;
     if (wpc < 1 || wpc > kPairWarps) wpc = 1;
@@ -696,6 +754,7 @@ static cudaError_t launch_strip(const PairDev& d, int sms, cudaStream_t stream) 
     const int strips = d.nprob * d.prob[0].nstrips;
     int grid = (strips + wpc - 1) / wpc;
     if (grid > sms * occ) grid = sms * occ;
+    if (grid * 32 * wpc > kPairSinkWords) grid = kPairSinkWords / (32 * wpc);
     pair_strip_kernel<K, STORE><<<grid, 32 * wpc, smem, stream>>>(d);
     return cudaGetLastError();
 }

@@ -87,7 +87,7 @@ struct Ctx {
     // batch
     DevBuf xs, ys, xoff, yoff, out, ws;
     // single pair
-    DevBuf px, py, pmg, carry, small, rows, outrev, codes, ry, vbuf, wave;
+    DevBuf px, py, pmg, carry, small, rows, outrev, codes, ry, vbuf, wave, sink;
     ~Ctx() {
         for (cudaEvent_t e : chunk_ev) cudaEventDestroy(e);
         if (copy_stream) cudaStreamDestroy(copy_stream);
@@ -167,6 +167,11 @@ struct PairPlan {
 // strip has a sub-partition to itself; strips start ~60 steps apart (lane
 // pipeline + hand-off); strips beyond the resident warps run in waves; more
 // resident strips than sub-partitions share issue slots.
+int batch_kmax() {
+    const int k = env_int("WLCS_BATCH_KMAX", 8);
+    return k >= 1 && k <= 8 ? k : 8;
+}
+
 int choose_k(const Ctx& c, int64_t W, int64_t rows_per_prob, int sigma, int nprob) {
     const int forced = env_int("WLCS_PAIR_K", 0);
     if (forced == 1 || forced == 2 || forced == 4 || forced == 8) return forced;
@@ -176,7 +181,7 @@ int choose_k(const Ctx& c, int64_t W, int64_t rows_per_prob, int sigma, int npro
     for (int K : {1, 2, 4, 8}) {
         const int smem = wlcs::pair_smem_bytes(K, sigma);
         if (smem > 200 * 1024) continue;
-        const double step = K == 1 ? 430 : K == 2 ? 490 : K == 4 ? 680 : 1100;
+        const double step = K == 1 ? 330 : K == 2 ? 363 : K == 4 ? 535 : 987;
         const double strips = double((W + 32 * K - 1) / (32 * K));
         const double total = strips * nprob;
         const double per_sm = std::min(32, (227 * 1024) / std::max(smem, 1));
@@ -201,7 +206,7 @@ void set_problem(wlcs::FillProblem& P, int64_t rows, uint32_t* pmg, int64_t cols
     P.nchunks = int((rows + 15) / 16);
     P.Mpad = int64_t(P.nchunks) * 16;
     P.Dpad = P.Mpad + 512;
-    P.cwords = ((int64_t(P.nchunks) + 3) & ~int64_t(3)) + 8;
+    P.cwords = ((int64_t(P.nchunks) + 3) & ~int64_t(3)) + 16;
 }
 
 bool use_split(int64_t rows, bool store) {
@@ -229,6 +234,8 @@ int pair_setup(Ctx& c, const uint8_t* d_row, int64_t rows, const uint8_t* d_col,
     uint16_t* map = reinterpret_cast<uint16_t*>(sb + 1024);
     uint32_t* sigma_dev = reinterpret_cast<uint32_t*>(sb + 1536);
     d.ticket = reinterpret_cast<uint32_t*>(sb + 1540);
+    WLCS_CUDA(c.sink.ensure(size_t(wlcs::kPairSinkWords) * 4));
+    d.sink = c.sink.as<uint32_t>();
     unsigned long long* zeros = reinterpret_cast<unsigned long long*>(sb + 1544);
     d.safe16 = reinterpret_cast<const uint4*>(sb + 2048);  // zeroed below
     int sigma = 0;
@@ -438,6 +445,7 @@ int batch_device(Ctx& c, const uint8_t* d_xs, const uint64_t* d_xoff, const uint
     d.out = d_out;
     d.pairs = uint32_t(pairs);
     d.pm_bytes = pm_bytes;
+        d.kmax = batch_kmax();
     if (c.timing && !c.ev0) {
         WLCS_CUDA(cudaEventCreate(&c.ev0));
         WLCS_CUDA(cudaEventCreate(&c.ev1));
@@ -516,6 +524,7 @@ int batch_host_pipelined(Ctx& c, const uint8_t* xs, const uint64_t* x_off, const
         d.out = c.out.as<uint32_t>() + p0[k];
         d.pairs = uint32_t(p0[k + 1] - p0[k]);
         d.pm_bytes = pm_bytes;
+        d.kmax = batch_kmax();
         const bool ends = k == 0 || k == nchunks - 1;
         WLCS_CUDA(wlcs::batch_launch(d, c.ws.as<uint8_t>() + ws_off[k], c.sms, s,
                                      (c.timing && ends && k == 0) ? c.ev0 : nullptr,
@@ -804,7 +813,7 @@ int wlcs_colsplit_inbox_words(size_t m, size_t* words) {
     if (!words) return fail(WLCS_E_INVALID_ARGUMENT, "words is NULL");
     const size_t rows = m - m / 2;  // the larger half
     const size_t nch = (rows + 15) / 16;
-    *words = ((nch + 3) & ~size_t(3)) + 8;
+    *words = ((nch + 3) & ~size_t(3)) + 16;
     return WLCS_OK;
 }
 
@@ -837,6 +846,8 @@ int wlcs_colsplit_fill(const uint8_t* x, size_t m, const uint8_t* y, size_t n, s
     uint16_t* map = reinterpret_cast<uint16_t*>(sb + 1024);
     d.ticket = reinterpret_cast<uint32_t*>(sb + 1540);
     d.safe16 = reinterpret_cast<const uint4*>(sb + 2048);
+    WLCS_CUDA(c->sink.ensure(size_t(wlcs::kPairSinkWords) * 4));
+    d.sink = c->sink.as<uint32_t>();
     int sigma = 0;
     WLCS_CUDA(wlcs::pair_prepare(d, reinterpret_cast<uint32_t*>(sb), map,
                                  reinterpret_cast<uint32_t*>(sb + 1536), c->stream, &sigma));

@@ -19,6 +19,7 @@ struct BatchDev {
     uint32_t* out;         // pairs lengths
     uint32_t pairs;
     int pm_bytes;          // shared-memory bytes for match masks per warp
+    int kmax;              // largest words-per-lane K of a lane shape (<= 8)
     // filled by batch_launch from the workspace
     uint32_t* keys_in;
     uint32_t* vals_in;
@@ -54,7 +55,7 @@ struct FillProblem {
     int nstrips;            // ceil(W / (32 K))
     int nchunks;            // 16-row chunks of the row string
     uint32_t* carry;        // [nstrips][cwords] carry words, zero-initialised
-    int64_t cwords;         // carry-row stride: round_up(nchunks, 4) + 8
+    int64_t cwords;         // carry-row stride: round_up(nchunks, 4) + 16
     uint32_t* v_out;        // optional: final V words [>= W]
     unsigned long long* zeros;  // optional: LCS accumulator
     uint32_t* rows_out;     // optional: bit rows, diagonal layout (traceback)
@@ -72,13 +73,18 @@ struct PairDev {
     FillProblem prob[2];
     int nprob;
     uint32_t code_stride;   // smem bytes per code record (set by pair_fill)
+    uint32_t pm_warp_bytes; // smem bytes of the match masks (set by pair_fill)
     int walk_pm_smem;       // walk keeps the match-mask table in shared memory
     const uint8_t* colp0;   // column string of problem 0 (alphabet scan)
     const uint16_t* map;    // 256 byte -> code map of the column alphabet
     int sigma;              // codes incl. the zero row
     uint32_t* ticket;       // strip ticket counter
+    uint32_t* sink;         // scratch the strip kernel's non-publishing lanes store to
+                            // (>= kPairSinkWords words)
     const uint4* safe16;    // 16 zero bytes in device memory
 };
+
+constexpr int kPairSinkWords = 1 << 20;  // >= grid * block threads of the strip kernel
 
 cudaError_t pair_prepare(PairDev& d, uint32_t* present256, uint16_t* map256, uint32_t* sigma_dev,
                          cudaStream_t stream, int* sigma_host);

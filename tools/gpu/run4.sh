@@ -1,2 +1,4 @@
-timeout 300 python bench.py --config c3 --steps 1 --warmup 0 > gpurun_out/b.json 2>&1 && \
-timeout 600 ncu --set full --import-source on --clock-control none -k regex:pair_walk -c 1 -f -o gpurun_out/walk python bench.py --config c3 --steps 1 --warmup 0 > /dev/null 2>&1; ls gpurun_out/walk*
+python tools/handoff_probe.py 400000 || exit 1
+ncu --set full --import-source on --clock-control none -k regex:pair_strip --launch-skip 6 -c 1 -f -o gpurun_out/consumer python tools/handoff_probe.py 400000 > /dev/null 2>&1
+ncu --set full --import-source on --clock-control none -k regex:pair_strip --launch-skip 0 -c 1 -f -o gpurun_out/solo4 python tools/handoff_probe.py 400000 > /dev/null 2>&1
+ls gpurun_out/*.ncu-rep
