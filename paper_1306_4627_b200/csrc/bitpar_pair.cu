@@ -118,14 +118,6 @@ __device__ __forceinline__ uint32_t ld_relaxed_gpu(const uint32_t* p) {
     asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
-__device__ __forceinline__ uint4 ld_relaxed_gpu_v4(const uint32_t* p) {
-    uint4 v;
-    asm volatile("ld.relaxed.gpu.global.v4.u32 {%0, %1, %2, %3}, [%4];"
-                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-                 : "l"(p)
-                 : "memory");
-    return v;
-}
 // System-scope variants for the carry words that cross GPUs (column split:
 // the producer writes into the consumer's memory over NVLink / P2P).
 __device__ __forceinline__ uint32_t ld_relaxed_sys(const uint32_t* p) {
@@ -140,9 +132,6 @@ __device__ __forceinline__ uint4 ld_relaxed_sys_v4(const uint32_t* p) {
                  : "l"(p)
                  : "memory");
     return v;
-}
-__device__ __forceinline__ void st_relaxed_sys(uint32_t* p, uint32_t v) {
-    asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 // L2-only (cache-global) vector load for polling self-validating words: a
 // weak load that always goes to L2, re-issued because the asm is volatile;
@@ -166,9 +155,6 @@ __device__ __forceinline__ void st_relaxed_gpu_nb(uint32_t* p, uint32_t v) {
 }
 __device__ __forceinline__ void st_relaxed_sys_nb(uint32_t* p, uint32_t v) {
     asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v));
-}
-__device__ __forceinline__ void st_relaxed_gpu(uint32_t* p, uint32_t v) {
-    asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
 constexpr uint32_t kCarryValid = 0x10000u;  // carry words: valid flag | 16-row mask
@@ -399,188 +385,173 @@ __global__ void __launch_bounds__(32, 1) pair_strip_kernel(PairDev d) {
     }
 }
 
-// Exact reference traceback over stored bit rows, one warp.
-// out receives the subsequence in REVERSE order; *out_len its length.
+// ---- exact reference traceback over the stored bit rows ------------------
 //
-// The walk is sequential (row i's decision sets the column for row i-1) and
-// latency-bound.  The warp works in blocks of 32 rows: every lane prepares,
-// for one row, a window of kWalkWords words at and below a predicted column
-// word in shared memory -- the event bits E = PM | ~V (match or Up), the
-// match bits PM, and for each word the position/type of the highest event
-// in the words below it -- so that lane 0's per-row step is three independent
-// LDS plus a handful of 32-bit ALU ops, with no data-dependent loop.  The
-// preparation of block b+1 is issued before lane 0 walks block b, so the
-// DRAM latency of the bit rows overlaps the walk.  A row whose next event
-// lies below the window is searched in global memory (rare).
-constexpr int kWalkWords = 8;
+// Row step: the reference walk (serial.cpp:44-58 with cell.hpp:30-38) inside
+// row i, entered at column j, leaves the row at
+//   j' = h + 1 - diag,  h = highest set bit <= j-1 of E = PM[x_i] | ~V_i,
+//   diag = bit h of PM[x_i]   (no set bit: Left to column 0, j' = 0)
+// and emits x_i iff diag.  j' is a monotone (non-decreasing) function of j,
+// hence so is the exit column of any block of rows: two walks that meet stay
+// together, and a walk entering between two walks that met leaves with them.
+//
+// Parallel walk (replaces the latency-bound serial walk, one row at a time):
+//  1. speculate: every block of kWalkRows rows is walked, in parallel, from
+//     kWalkCand candidate entry columns spaced kWalkStride apart around the
+//     column where the path would cross if it followed the diagonal;
+//  2. resolve (one thread, bottom block first): the true entry of block k is
+//     the exit of block k-1; if it lies between two candidates whose walks
+//     left the block at the same column, that column is the exit (O(1)),
+//     otherwise the block is walked from the true entry (rare);
+//  3. emit: every block is walked again, in parallel, from its true entry,
+//     flagging the rows that emit;
+//  4. the flagged row bytes are compacted in row order (forward string).
+constexpr int kWalkRows = 256;
+constexpr int kWalkCand = 128;   // candidates per block (4 warps)
+constexpr int kWalkStride = 16;  // columns between candidates
 
 template <int K>
-__device__ __noinline__ int64_t walk_row_global(const FillProblem& P, const uint16_t* map,
-                                                uint8_t xq, int64_t q, int64_t j, bool* diag) {
+__device__ __forceinline__ uint32_t walk_code(const FillProblem& P, int64_t q) {
+    const uint32_t* c32 = reinterpret_cast<const uint32_t*>(P.coded);
+    const int64_t r = q & 15, ch = q >> 4;
+    return c32[((r >> 2) * P.plane + ch * P.cstride) * 4 + (r & 3)];
+}
+
+// Column entering row q-1 (0-based q: DP row i = q + 1) from column j of row
+// i; *diag = emission.
+template <int K>
+__device__ __forceinline__ int64_t walk_step(const FillProblem& P, uint32_t code, int64_t q,
+                                             int64_t j, uint32_t* diag) {
+    *diag = 0;
+    if (j <= 0) return 0;
     int64_t w = (j - 1) >> 5;
-    const uint32_t* pmrow = P.pmg + int64_t(map[xq]) * P.W;
     uint32_t mask = (2u << ((j - 1) & 31)) - 1u;
-    for (;; --w, mask = 0xffffffffu) {
+    const uint32_t* pmrow = P.pmg + int64_t(code) * P.W;
+    for (;;) {
         const uint32_t pmw = __ldg(pmrow + w);
         const uint32_t e = (pmw | ~P.rows_out[pair_row_index(q, w, K, P.Dpad)]) & mask;
         if (e) {
             const int b = 31 - __clz(e);
             *diag = (pmw >> b) & 1u;
-            return w * 32 + b + 1 - (*diag ? 1 : 0);
+            return w * 32 + b + 1 - int64_t(*diag);
         }
-        if (w == 0) {
-            *diag = false;
-            return 0;  // Left all the way to column 0
-        }
+        if (w == 0) return 0;
+        --w;
+        mask = 0xffffffffu;
     }
 }
 
+__device__ __forceinline__ int64_t walk_guess(int64_t top_i, int64_t M, int64_t N) {
+    return (top_i * N + M / 2) / M;  // column of the diagonal at DP row top_i
+}
+__device__ __forceinline__ int64_t walk_cand(int64_t guess, int l, int64_t N) {
+    const int64_t c = guess + int64_t(l - kWalkCand / 2) * kWalkStride;
+    return c < 0 ? 0 : (c > N ? N : c);
+}
+
+// 1. one CTA (kWalkCand threads) per block of rows
 template <int K>
-__global__ void __launch_bounds__(32) pair_walk_kernel(PairDev d, const uint8_t* x, uint8_t* out,
-                                                       unsigned long long* out_len) {
-    __shared__ uint32_t se[2][32][kWalkWords], sp[2][32][kWalkWords];
-    __shared__ int32_t sv[2][32][kWalkWords];  // (pos*2 + diag) of the highest event below word s
-    __shared__ uint8_t sx[2][32];
+__global__ void __launch_bounds__(kWalkCand) walk_spec_kernel(PairDev d, int32_t* exits) {
+    __shared__ uint32_t codes[kWalkRows];
     const FillProblem& P = d.prob[0];
-    const int lane = int(threadIdx.x);
-    const int64_t W = P.W;
-    // match masks: the whole table in shared memory when it fits (pm_smem)
-    extern __shared__ __align__(16) uint32_t spm[];
-    const bool pm_smem = d.walk_pm_smem != 0;
-    if (pm_smem) {
-        for (int64_t k = lane; k < int64_t(d.sigma) * W; k += 32) spm[k] = __ldg(P.pmg + k);
-        __syncwarp();
+    const int64_t M = P.rows, N = P.cols;
+    const int64_t k = blockIdx.x;
+    const int64_t top = M - k * kWalkRows;  // DP row of the block's first (bottom) row
+    const int64_t lo = top - kWalkRows > 0 ? top - kWalkRows : 0;
+    for (int64_t i = top - threadIdx.x; i > lo; i -= blockDim.x)
+        codes[top - i] = walk_code<K>(P, i - 1);
+    __syncthreads();
+    int64_t j = walk_cand(walk_guess(top, M, N), int(threadIdx.x), N);
+    for (int64_t i = top; i > lo && j > 0; --i) {
+        uint32_t dg;
+        j = walk_step<K>(P, codes[top - i], i - 1, j, &dg);
     }
-    auto pm_word = [&](uint32_t code, int64_t w) -> uint32_t {
-        return pm_smem ? spm[int64_t(code) * W + w] : __ldg(P.pmg + int64_t(code) * W + w);
-    };
-    // stage 1 (before lane 0 walks the current block): the row byte, its code
-    // and the raw V words of row ibase-1-lane, words wlo .. wlo+7 -- loads
-    // only, nothing consumes them until stage 2
-    uint32_t rv[kWalkWords];
-    uint32_t rcode = 0;
-    uint8_t rx = 0;
-    const uint32_t* coded32 = reinterpret_cast<const uint32_t*>(P.coded);
-    auto fetch = [&](int64_t ibase, int64_t wlo) {
-        const int64_t q = ibase - 1 - lane;
-        rcode = 0;
-#pragma unroll
-        for (int s = 0; s < kWalkWords; ++s) rv[s] = 0xffffffffu;
-        if (q >= 0) {
-            rx = x[q];
-            const int64_t r = q & 15, ch = q >> 4;
-            rcode = coded32[((r >> 2) * P.plane + ch * P.cstride) * 4 + (r & 3)];
-#pragma unroll
-            for (int s = 0; s < kWalkWords; ++s) {
-                const int64_t w = wlo + s;
-                if (w < W) rv[s] = P.rows_out[pair_row_index(q, w, K, P.Dpad)];
+    exits[k * kWalkCand + threadIdx.x] = int32_t(j);
+}
+
+// 2. one thread; entry[k] = true entry column of block k
+template <int K>
+__global__ void walk_resolve_kernel(PairDev d, const int32_t* exits, int32_t* entry,
+                                    uint32_t* misses) {
+    const FillProblem& P = d.prob[0];
+    const int64_t M = P.rows, N = P.cols;
+    const int64_t nb = (M + kWalkRows - 1) / kWalkRows;
+    int64_t j = N;
+    uint32_t miss = 0;
+    for (int64_t k = 0; k < nb; ++k) {
+        entry[k] = int32_t(j);
+        const int64_t top = M - k * kWalkRows;
+        const int64_t lo = top - kWalkRows > 0 ? top - kWalkRows : 0;
+        const int64_t g = walk_guess(top, M, N);
+        const int32_t* ex = exits + k * kWalkCand;
+        int64_t next = -1;
+        // bracketing candidates (candidate columns are non-decreasing in l)
+        const int64_t l0 = (j - walk_cand(g, 0, N)) / kWalkStride;
+        for (int64_t l = l0 - 1; l <= l0 + 1 && next < 0; ++l) {
+            if (l < 0 || l >= kWalkCand) continue;
+            const int64_t ca = walk_cand(g, int(l), N);
+            if (ca == j) next = ex[l];
+            else if (l + 1 < kWalkCand && ca < j && j < walk_cand(g, int(l + 1), N) &&
+                     ex[l] == ex[l + 1])
+                next = ex[l];
+        }
+        if (next < 0) {  // outside the window or the bracket did not merge
+            ++miss;
+            next = j;
+            for (int64_t i = top; i > lo && next > 0; --i) {
+                uint32_t dg;
+                next = walk_step<K>(P, walk_code<K>(P, i - 1), i - 1, next, &dg);
             }
         }
-    };
-    // stage 2: event words, match words and the below-word summaries
-    auto commit = [&](int buf, int64_t wlo) {
-        int32_t prev = -1;
-#pragma unroll
-        for (int s = 0; s < kWalkWords; ++s) {
-            const int64_t w = wlo + s;
-            const uint32_t pm = w < W ? pm_word(rcode, w) : 0u;
-            const uint32_t ev = pm | ~rv[s];
-            se[buf][lane][s] = ev;
-            sp[buf][lane][s] = pm;
-            sv[buf][lane][s] = prev;
-            if (ev) {
-                const int b = 31 - __clz(ev);
-                prev = (s * 32 + b) * 2 + int((pm >> b) & 1u);
-            }
-        }
-        sx[buf][lane] = rx;
-    };
-    int64_t i = P.rows, j = P.cols;  // 1-based DP coordinates
-    unsigned long long len = 0;
-    int buf = 0;
-    // window: the kWalkWords words at and below the column word at fetch time
-    // (j only decreases; 256 columns cover the drop over this block and the
-    // next one for any path that is not a long run of Left moves)
-    auto window_lo = [&](int64_t jtop) {
-        const int64_t lo = ((jtop - 1) >> 5) - (kWalkWords - 1);
-        return lo < 0 ? int64_t(0) : lo;
-    };
-    int64_t wlo = window_lo(j);
-    if (i > 0 && j > 0) {
-        fetch(i, wlo);
-        commit(0, wlo);
+        j = next;
     }
-    __syncwarp();
-    while (i > 0 && j > 0) {
-        const int64_t wlo_next = window_lo(j);
-        fetch(i - 32, wlo_next);
-        if (lane == 0) {
-            const int rows = i < 32 ? int(i) : 32;
-            const int64_t jbase = 32 * wlo;
-            int32_t jl = int32_t(j - jbase);  // local column, 1 .. 32*kWalkWords
-            uint8_t* o = out + len;
-            int n = 0;
-            int l = 0;
-            bool ended = false;
-            // one row; returns false when the walk has ended
-            auto step = [&](int r) -> bool {
-                const int32_t jm = jl - 1;
-                const int sw = jm >> 5;  // < 0: below the window (rare path)
-                const int sc = sw < 0 ? 0 : sw;
-                const uint32_t e = se[buf][r][sc] & ((2u << (jm & 31)) - 1u);
-                const uint32_t pw = sp[buf][r][sc];
-                const int32_t pv = sv[buf][r][sc];
-                const int b = 31 - __clz(e);
-                int32_t pos = e ? sc * 32 + b : pv >> 1;
-                int32_t dg = e ? int32_t((pw >> b) & 1u) : (pv & 1);
-                if (sw < 0 || (e == 0u && pv < 0)) {  // rare: below the window or no event
-                    if (jbase + jl <= 0) return false;  // column 0: the walk has ended
-                    if (wlo == 0 && sw >= 0) {          // no event down to column 0
-                        jl = int32_t(-jbase);
-                        return false;
-                    }
-                    const int64_t jq = sw < 0 ? jbase + jl : jbase + 32 * sc;
-                    bool dgb = false;
-                    const int64_t jn = walk_row_global<K>(P, d.map, sx[buf][r], i - 1 - r, jq, &dgb);
-                    pos = int32_t(jn - jbase) - (dgb ? 0 : 1);
-                    dg = dgb ? 1 : 0;
-                }
-                o[n] = sx[buf][r];  // kept only if dg (the next emit overwrites it)
-                n += dg;
-                jl = pos + 1 - dg;
-                return true;
-            };
-            if (rows == 32) {
-#pragma unroll
-                for (int r = 0; r < 32; ++r) {
-                    if (!step(r)) {
-                        ended = true;
-                        l = r + 1;
-                        break;
-                    }
-                }
-                if (!ended) l = 32;
-            } else {
-                for (; l < rows; ++l) {
-                    if (!step(l)) {
-                        ++l;
-                        break;
-                    }
-                }
-            }
-            len += n;
-            j = jbase + jl;
-            if (j < 0) j = 0;
-            i -= l;
-        }
-        i = __shfl_sync(kFullMask, i, 0);
-        j = __shfl_sync(kFullMask, j, 0);
-        buf ^= 1;
-        wlo = wlo_next;
-        commit(buf, wlo);
-        __syncwarp();
+    *misses = miss;
+}
+
+// 3. one thread per block: flags[q] = 1 iff row q emits; counts[k]
+template <int K>
+__global__ void walk_emit_kernel(PairDev d, const int32_t* entry, uint8_t* flags,
+                                 uint32_t* counts) {
+    const FillProblem& P = d.prob[0];
+    const int64_t M = P.rows;
+    const int64_t nb = (M + kWalkRows - 1) / kWalkRows;
+    const int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (k >= nb) return;
+    const int64_t top = M - k * kWalkRows;
+    const int64_t lo = top - kWalkRows > 0 ? top - kWalkRows : 0;
+    int64_t j = entry[k];
+    uint32_t n = 0;
+    for (int64_t i = top; i > lo; --i) {
+        uint32_t dg = 0;
+        if (j > 0) j = walk_step<K>(P, walk_code<K>(P, i - 1), i - 1, j, &dg);
+        flags[i - 1] = uint8_t(dg);
+        n += dg;
     }
-    if (lane == 0) *out_len = len;
+    counts[k] = n;
+}
+
+// 4a. one thread: output offsets (forward order = blocks from the top rows)
+__global__ void walk_scan_kernel(const uint32_t* counts, int64_t nb, uint32_t* offsets,
+                                 unsigned long long* total) {
+    unsigned long long run = 0;
+    for (int64_t k = nb - 1; k >= 0; --k) {
+        offsets[k] = uint32_t(run);
+        run += counts[k];
+    }
+    *total = run;
+}
+
+// 4b. one thread per block writes its emitted bytes in row order
+__global__ void walk_write_kernel(const uint8_t* x, int64_t M, const uint8_t* flags,
+                                  const uint32_t* offsets, uint8_t* out) {
+    const int64_t nb = (M + kWalkRows - 1) / kWalkRows;
+    const int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (k >= nb) return;
+    const int64_t top = M - k * kWalkRows;
+    const int64_t lo = top - kWalkRows > 0 ? top - kWalkRows : 0;
+    uint8_t* o = out + offsets[k];
+    for (int64_t q = lo; q < top; ++q)
+        if (flags[q]) *o++ = x[q];
 }
 
 // ---- bidirectional split (Hirschberg's lemma) -----------------------------
@@ -773,24 +744,36 @@ cudaError_t pair_fill(const PairDev& d, int K, bool store, int sms, cudaStream_t
     }
 }
 
-cudaError_t pair_walk(const PairDev& d, int K, const uint8_t* x, uint8_t* out_rev,
-                      unsigned long long* out_len, cudaStream_t stream) {
-    PairDev dw = d;
-    const size_t pm_bytes = size_t(d.sigma) * size_t(d.prob[0].W) * 4;
-    dw.walk_pm_smem = pm_bytes <= 200 * 1024 ? 1 : 0;
-    const int smem = dw.walk_pm_smem ? int(pm_bytes) : 0;
-    auto launch = [&](auto kern) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             smem);
-        if (e != cudaSuccess) return e;
-        kern<<<1, 32, smem, stream>>>(dw, x, out_rev, out_len);
+size_t pair_walk_scratch_bytes(int64_t rows) {
+    const int64_t nb = (rows + kWalkRows - 1) / kWalkRows;
+    return size_t(nb) * kWalkCand * 4 + size_t(nb) * 12 + size_t(rows) + 64;
+}
+
+cudaError_t pair_walk(const PairDev& d, int K, const uint8_t* x, uint8_t* out,
+                      unsigned long long* out_len, void* scratch, uint32_t* misses,
+                      cudaStream_t stream) {
+    const int64_t M = d.prob[0].rows;
+    const int64_t nb = (M + kWalkRows - 1) / kWalkRows;
+    int32_t* exits = static_cast<int32_t*>(scratch);
+    int32_t* entry = exits + nb * kWalkCand;
+    uint32_t* counts = reinterpret_cast<uint32_t*>(entry + nb);
+    uint32_t* offsets = counts + nb;
+    uint8_t* flags = reinterpret_cast<uint8_t*>(offsets + nb);
+    const int tb = 128;
+    const int eb = int((nb + tb - 1) / tb);
+    auto run = [&](auto spec, auto resolve, auto emit) {
+        spec<<<int(nb), kWalkCand, 0, stream>>>(d, exits);
+        resolve<<<1, 1, 0, stream>>>(d, exits, entry, misses);
+        emit<<<eb, tb, 0, stream>>>(d, entry, flags, counts);
+        walk_scan_kernel<<<1, 1, 0, stream>>>(counts, nb, offsets, out_len);
+        walk_write_kernel<<<eb, tb, 0, stream>>>(x, M, flags, offsets, out);
         return cudaGetLastError();
     };
     switch (K) {
-        case 1: return launch(pair_walk_kernel<1>);
-        case 2: return launch(pair_walk_kernel<2>);
-        case 4: return launch(pair_walk_kernel<4>);
-        case 8: return launch(pair_walk_kernel<8>);
+        case 1: return run(walk_spec_kernel<1>, walk_resolve_kernel<1>, walk_emit_kernel<1>);
+        case 2: return run(walk_spec_kernel<2>, walk_resolve_kernel<2>, walk_emit_kernel<2>);
+        case 4: return run(walk_spec_kernel<4>, walk_resolve_kernel<4>, walk_emit_kernel<4>);
+        case 8: return run(walk_spec_kernel<8>, walk_resolve_kernel<8>, walk_emit_kernel<8>);
         default: return cudaErrorInvalidValue;
     }
 }

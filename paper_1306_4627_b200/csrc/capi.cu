@@ -87,7 +87,7 @@ struct Ctx {
     // batch
     DevBuf xs, ys, xoff, yoff, out, ws;
     // single pair
-    DevBuf px, py, pmg, carry, small, rows, outrev, codes, ry, vbuf, wave, sink;
+    DevBuf px, py, pmg, carry, small, rows, outrev, codes, ry, vbuf, wave, sink, walk;
     ~Ctx() {
         for (cudaEvent_t e : chunk_ev) cudaEventDestroy(e);
         if (copy_stream) cudaStreamDestroy(copy_stream);
@@ -662,7 +662,10 @@ int wlcs_subsequence(const uint8_t* x, size_t m, const uint8_t* y, size_t n,
     WLCS_CUDA(c->outrev.ensure(maxlen + 16));
     unsigned long long* zeros_dev = pair_zeros_ptr(*c);
     unsigned long long* dlen = zeros_dev + 1;
-    WLCS_CUDA(wlcs::pair_walk(plan.d, plan.K, dx, c->outrev.as<uint8_t>(), dlen, c->stream));
+    WLCS_CUDA(c->walk.ensure(wlcs::pair_walk_scratch_bytes(int64_t(m))));
+    uint32_t* dmiss = reinterpret_cast<uint32_t*>(zeros_dev + 2);
+    WLCS_CUDA(wlcs::pair_walk(plan.d, plan.K, dx, c->outrev.as<uint8_t>(), dlen, c->walk.p,
+                              dmiss, c->stream));
     unsigned long long len = 0, zeros = 0;
     WLCS_CUDA(cudaMemcpyAsync(&len, dlen, 8, cudaMemcpyDeviceToHost, c->stream));
     WLCS_CUDA(cudaMemcpyAsync(&zeros, zeros_dev, 8, cudaMemcpyDeviceToHost, c->stream));
@@ -675,9 +678,7 @@ int wlcs_subsequence(const uint8_t* x, size_t m, const uint8_t* y, size_t n,
     if (len > cap)
         return fail(WLCS_E_INVALID_ARGUMENT, "output buffer holds " + std::to_string(cap) +
                                                  " bytes, subsequence has " + std::to_string(len));
-    std::vector<uint8_t> rev(len);
-    if (len) WLCS_CUDA(cudaMemcpy(rev.data(), c->outrev.p, len, cudaMemcpyDeviceToHost));
-    for (size_t k = 0; k < len; ++k) out[k] = rev[len - 1 - k];
+    if (len) WLCS_CUDA(cudaMemcpy(out, c->outrev.p, len, cudaMemcpyDeviceToHost));
     return WLCS_OK;
 }
 

@@ -74,7 +74,6 @@ struct PairDev {
     int nprob;
     uint32_t code_stride;   // smem bytes per code record (set by pair_fill)
     uint32_t pm_warp_bytes; // smem bytes of the match masks (set by pair_fill)
-    int walk_pm_smem;       // walk keeps the match-mask table in shared memory
     const uint8_t* colp0;   // column string of problem 0 (alphabet scan)
     const uint16_t* map;    // 256 byte -> code map of the column alphabet
     int sigma;              // codes incl. the zero row
@@ -98,8 +97,11 @@ cudaError_t pair_split_combine(const uint32_t* vf, const uint32_t* vr, int64_t W
                                uint32_t* scratch, unsigned long long* best, cudaStream_t stream);
 int pair_smem_bytes(int K, int sigma);
 cudaError_t pair_fill(const PairDev& d, int K, bool store, int sms, cudaStream_t stream);
-cudaError_t pair_walk(const PairDev& d, int K, const uint8_t* x, uint8_t* out_rev,
-                      unsigned long long* out_len, cudaStream_t stream);
+size_t pair_walk_scratch_bytes(int64_t rows);
+// Exact traceback; out receives the subsequence in FORWARD order.
+cudaError_t pair_walk(const PairDev& d, int K, const uint8_t* x, uint8_t* out,
+                      unsigned long long* out_len, void* scratch, uint32_t* misses,
+                      cudaStream_t stream);
 
 }  // namespace wlcs
 
