@@ -86,6 +86,65 @@ Length lcs_length(const Sequence& x, const Sequence& y,
 Sequence lcs_subsequence(const Sequence& x, const Sequence& y,
                          std::size_t memory_budget = kDefaultMemoryBudget);
 
+/// Which recurrence case produced a cell (cell.hpp:13-25).
+enum class Arrow : std::uint8_t { Diag = 0, Up = 1, Left = 2 };
+
+/// (M+1) x (N+1) prefix LCS lengths, row-major; same layout and accessors as
+/// the reference's DpTable (tables.hpp:20-45).
+class DpTable {
+public:
+    DpTable() = default;
+    DpTable(std::size_t m, std::size_t n) : rows_(m + 1), cols_(n + 1), cells_(rows_ * cols_, 0) {}
+    std::size_t rows() const noexcept { return rows_; }
+    std::size_t cols() const noexcept { return cols_; }
+    Length at(std::size_t i, std::size_t j) const { return cells_[i * cols_ + j]; }
+    Length& at(std::size_t i, std::size_t j) { return cells_[i * cols_ + j]; }
+    Length* data() noexcept { return cells_.data(); }
+    const Length* data() const noexcept { return cells_.data(); }
+    std::size_t stride() const noexcept { return cols_; }
+    Length final_length() const { return cells_.empty() ? 0 : cells_.back(); }
+    friend bool operator==(const DpTable&, const DpTable&) = default;
+
+private:
+    std::size_t rows_ = 0, cols_ = 0;
+    std::vector<Length> cells_;
+};
+
+/// M x N arrows, 1-based accessors; the reference's BacktrackTable
+/// (tables.hpp:49-71).
+class BacktrackTable {
+public:
+    BacktrackTable() = default;
+    BacktrackTable(std::size_t m, std::size_t n) : rows_(m), cols_(n), cells_(m * n, Arrow::Left) {}
+    std::size_t rows() const noexcept { return rows_; }
+    std::size_t cols() const noexcept { return cols_; }
+    Arrow at(std::size_t i, std::size_t j) const { return cells_[(i - 1) * cols_ + (j - 1)]; }
+    Arrow& at(std::size_t i, std::size_t j) { return cells_[(i - 1) * cols_ + (j - 1)]; }
+    Arrow* data() noexcept { return cells_.data(); }
+    const Arrow* data() const noexcept { return cells_.data(); }
+    std::size_t stride() const noexcept { return cols_; }
+    friend bool operator==(const BacktrackTable&, const BacktrackTable&) = default;
+
+private:
+    std::size_t rows_ = 0, cols_ = 0;
+    std::vector<Arrow> cells_;
+};
+
+struct FillResult {
+    DpTable dp;
+    BacktrackTable back;
+};
+
+/// lcs_fill_serial (serial.hpp:21-22) with the tables filled on the device:
+/// identical DpTable / BacktrackTable contents, same CapacityError.
+FillResult lcs_fill_serial(const Sequence& x, const Sequence& y,
+                           std::size_t memory_budget = kDefaultMemoryBudget);
+
+/// traceback (serial.hpp:30): walks the arrow table from (i, j); forward
+/// order; std::out_of_range when (i, j) is outside the table.  Host code (it
+/// reads a host table, exactly like the reference).
+Sequence traceback(const BacktrackTable& back, const Sequence& x, std::size_t i, std::size_t j);
+
 /// Lengths of many independent pairs (xs[k], ys[k]).
 std::vector<Length> lcs_length_batch(const std::vector<Sequence>& xs,
                                      const std::vector<Sequence>& ys);

@@ -180,6 +180,16 @@ int wlcs_colsplit_fill(const uint8_t* x, size_t m, const uint8_t* y, size_t n, s
                        uint32_t* d_out_fwd, const uint32_t* d_in_rev, uint32_t* d_out_rev,
                        uint32_t* v_fwd, uint32_t* v_rev);
 
+/* The reference's full tables, filled on the device:
+ * replaces lcs_fill_serial / lcs_fill_parallel's FillResult
+ * (include/wavelcs/serial.hpp:21-22, parallel.hpp:92-93) for callers that
+ * need the tables themselves.  dp: (m+1)*(n+1) uint32 cells, row-major,
+ * layout of DpTable (tables.hpp:20-45); back: m*n arrows (Diag 0 / Up 1 /
+ * Left 2), layout of BacktrackTable (tables.hpp:49-71).  Host buffers.
+ * memory_budget is checked exactly as check_capacity (tables.cpp:9-24). */
+int wlcs_fill_tables(const uint8_t* x, size_t m, const uint8_t* y, size_t n,
+                     size_t memory_budget, uint32_t* dp, uint8_t* back);
+
 /* Single-process multi-GPU conveniences, devices 0..n_gpus-1
  * of the calling process, one host thread per device:
  *  - wlcs_length_batch_multi: pairs sharded into contiguous ranges balanced by

@@ -121,6 +121,7 @@ lib.wlcs_device_free.argtypes = [_vp]
 lib.wlcs_ipc_handle.argtypes = [_vp, ctypes.c_char_p]
 lib.wlcs_ipc_open.argtypes = [ctypes.c_char_p, ctypes.POINTER(ctypes.c_void_p)]
 lib.wlcs_ipc_close.argtypes = [_vp]
+lib.wlcs_fill_tables.argtypes = [_vp, _sz, _vp, _sz, _sz, _vp, _vp]
 lib.wlcs_length_batch_multi.argtypes = [_vp, _u64p, _vp, _u64p, _sz, ctypes.c_int,
                                         ctypes.POINTER(ctypes.c_uint32)]
 lib.wlcs_length_strips.argtypes = [_vp, _sz, _vp, _sz, ctypes.c_int,
@@ -297,3 +298,15 @@ def lcs_length_strips(x, y, n_gpus: int) -> int:
     out = ctypes.c_uint32()
     _check(lib.wlcs_length_strips(xb, len(xb), yb, len(yb), n_gpus, ctypes.byref(out)))
     return int(out.value)
+
+
+def fill_tables(x, y, memory_budget: int = DEFAULT_MEMORY_BUDGET):
+    """The reference's FillResult (lcs_fill_serial, include/wavelcs/serial.hpp:
+    21-22) filled on the device: (dp uint32 (m+1, n+1), back uint8 (m, n))."""
+    xb, yb = _as_bytes(x), _as_bytes(y)
+    m, n = len(xb), len(yb)
+    dp = np.zeros((m + 1, n + 1), np.uint32)
+    back = np.zeros((m, n), np.uint8)
+    _check(lib.wlcs_fill_tables(xb, m, yb, n, memory_budget, dp.ctypes.data,
+                                back.ctypes.data if back.size else None))
+    return dp, back

@@ -554,6 +554,57 @@ __global__ void walk_write_kernel(const uint8_t* x, int64_t M, const uint8_t* fl
         if (flags[q]) *o++ = x[q];
 }
 
+// ---- the reference's full tables from the stored bit rows ----------------
+// DpTable (tables.hpp:20-45): (M+1) x (N+1) uint32, row-major, row/col 0 = 0,
+//   c[i][j] = zero bits of V_i below column j   (prefix popcount)
+// BacktrackTable (tables.hpp:49-71): M x N arrows, (i-1)*N + (j-1):
+//   Diag (0) if x_i == y_j; else Up (1) iff bit j-1 of V_i is 0 (then
+//   c[i-1][j] > c[i][j-1]); else Left (2)  -- lcs_cell, cell.hpp:30-38.
+// One warp per DP row; a lane expands one 32-column word at a time.
+template <int K>
+__global__ void __launch_bounds__(32) tables_kernel(PairDev d, uint32_t* dp, uint8_t* back) {
+    const FillProblem& P = d.prob[0];
+    const int64_t N = P.cols, W = P.W;
+    const int64_t i = blockIdx.x;  // DP row 0..M
+    const int lane = int(threadIdx.x);
+    uint32_t* drow = dp + i * (N + 1);
+    if (lane == 0) drow[0] = 0;
+    if (i == 0) {
+        for (int64_t j = 1 + lane; j <= N; j += 32) drow[j] = 0;
+        return;
+    }
+    const int64_t q = i - 1;
+    const uint32_t code = walk_code<K>(P, q);
+    const uint32_t* pmrow = P.pmg + int64_t(code) * W;
+    uint8_t* brow = back + q * N;
+    uint32_t base = 0;  // zeros of the words before this chunk of 32 words
+    for (int64_t w0 = 0; w0 < W; w0 += 32) {
+        const int64_t w = w0 + lane;
+        const int64_t c0 = w * 32;  // first column (0-based) of the word
+        const int nbits = w < W ? int(N - c0 < 32 ? N - c0 : 32) : 0;
+        uint32_t v = 0xffffffffu, pm = 0;
+        if (nbits > 0) {
+            v = P.rows_out[pair_row_index(q, w, K, P.Dpad)];
+            pm = __ldg(pmrow + w);
+        }
+        const uint32_t valid = nbits >= 32 ? 0xffffffffu : ((1u << nbits) - 1u);
+        const uint32_t z = __popc(~v & valid);
+        uint32_t incl = z;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(kFullMask, incl, o);
+            if (lane >= o) incl += t;
+        }
+        const uint32_t before = base + incl - z;
+        for (int b = 0; b < nbits; ++b) {
+            const uint32_t below = (2u << b) - 1u;  // bits 0..b
+            drow[c0 + b + 1] = before + __popc(~v & below);
+            brow[c0 + b] = ((pm >> b) & 1u) ? uint8_t(0) : (((v >> b) & 1u) ? uint8_t(2) : uint8_t(1));
+        }
+        base += __shfl_sync(kFullMask, incl, 31);
+    }
+}
+
 // ---- bidirectional split (Hirschberg's lemma) -----------------------------
 // L = max_k  F[k] + R[k],  F[k] = c_top[mid][k] = zeros of Vf below k,
 // R[k] = LCS(x[mid:], y[k:]) = zeros of Vr below N - k (Vr: reversed strings).
@@ -776,6 +827,19 @@ cudaError_t pair_walk(const PairDev& d, int K, const uint8_t* x, uint8_t* out,
         case 8: return run(walk_spec_kernel<8>, walk_resolve_kernel<8>, walk_emit_kernel<8>);
         default: return cudaErrorInvalidValue;
     }
+}
+
+cudaError_t pair_tables(const PairDev& d, int K, uint32_t* dp, uint8_t* back,
+                        cudaStream_t stream) {
+    const int64_t rows = d.prob[0].rows + 1;
+    switch (K) {
+        case 1: tables_kernel<1><<<int(rows), 32, 0, stream>>>(d, dp, back); break;
+        case 2: tables_kernel<2><<<int(rows), 32, 0, stream>>>(d, dp, back); break;
+        case 4: tables_kernel<4><<<int(rows), 32, 0, stream>>>(d, dp, back); break;
+        case 8: tables_kernel<8><<<int(rows), 32, 0, stream>>>(d, dp, back); break;
+        default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
 }
 
 }  // namespace wlcs

@@ -1106,4 +1106,39 @@ int wlcs_length_strips(const uint8_t* x, size_t m, const uint8_t* y, size_t n, i
     return WLCS_OK;
 }
 
+// ------------------------------------------------------- full tables
+int wlcs_fill_tables(const uint8_t* x, size_t m, const uint8_t* y, size_t n,
+                     size_t memory_budget, uint32_t* dp, uint8_t* back) {
+    if (!dp || (m && n && !back)) return fail(WLCS_E_INVALID_ARGUMENT, "NULL output");
+    if ((m && !x) || (n && !y)) return fail(WLCS_E_INVALID_ARGUMENT, "NULL input");
+    int rc = capacity_check(m, n, memory_budget);
+    if (rc) return rc;
+    Ctx* c = nullptr;
+    rc = get_ctx(&c);
+    if (rc) return rc;
+    if (m == 0 || n == 0) {  // all-zero DpTable, empty BacktrackTable (serial.cpp:13-16)
+        std::memset(dp, 0, (m + 1) * (n + 1) * sizeof(uint32_t));
+        return WLCS_OK;
+    }
+    WLCS_CUDA(c->px.ensure(m + 16));
+    WLCS_CUDA(c->py.ensure(n + 16));
+    WLCS_CUDA(cudaMemcpyAsync(c->px.p, x, m, cudaMemcpyHostToDevice, c->stream));
+    WLCS_CUDA(cudaMemcpyAsync(c->py.p, y, n, cudaMemcpyHostToDevice, c->stream));
+    PairPlan plan;
+    rc = pair_setup(*c, c->px.as<uint8_t>(), int64_t(m), c->py.as<uint8_t>(), int64_t(n), true,
+                    plan);
+    if (rc) return rc;
+    WLCS_CUDA(wlcs::pair_fill(plan.d, plan.K, true, c->sms, c->stream));
+    const size_t dp_bytes = (m + 1) * (n + 1) * sizeof(uint32_t), back_bytes = m * n;
+    DevBuf tdp, tback;
+    WLCS_CUDA(tdp.ensure(dp_bytes));
+    WLCS_CUDA(tback.ensure(back_bytes));
+    WLCS_CUDA(wlcs::pair_tables(plan.d, plan.K, tdp.as<uint32_t>(), tback.as<uint8_t>(),
+                                c->stream));
+    WLCS_CUDA(cudaMemcpyAsync(dp, tdp.p, dp_bytes, cudaMemcpyDeviceToHost, c->stream));
+    WLCS_CUDA(cudaMemcpyAsync(back, tback.p, back_bytes, cudaMemcpyDeviceToHost, c->stream));
+    WLCS_CUDA(cudaStreamSynchronize(c->stream));
+    return WLCS_OK;
+}
+
 }  // extern "C"

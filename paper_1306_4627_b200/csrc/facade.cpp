@@ -55,6 +55,41 @@ Sequence lcs_subsequence(const Sequence& x, const Sequence& y, std::size_t memor
     return Sequence(std::move(buf));
 }
 
+FillResult lcs_fill_serial(const Sequence& x, const Sequence& y, std::size_t memory_budget) {
+    // capacity first, before any allocation (serial.cpp:12)
+    raise(wlcs_check_capacity(x.size(), y.size(), memory_budget));
+    FillResult out{DpTable(x.size(), y.size()), BacktrackTable(x.size(), y.size())};
+    if (x.empty() || y.empty()) return out;
+    raise(wlcs_fill_tables(bytes(x), x.size(), bytes(y), y.size(), memory_budget,
+                           out.dp.data(), reinterpret_cast<std::uint8_t*>(out.back.data())));
+    return out;
+}
+
+// serial.cpp:36-61 semantics.
+Sequence traceback(const BacktrackTable& back, const Sequence& x, std::size_t i, std::size_t j) {
+    if (i > back.rows() || j > back.cols())
+        throw std::out_of_range("traceback: position (" + std::to_string(i) + ", " +
+                                std::to_string(j) + ") outside " + std::to_string(back.rows()) +
+                                " x " + std::to_string(back.cols()) + " table");
+    std::string reversed;
+    while (i > 0 && j > 0) {
+        switch (back.at(i, j)) {
+            case Arrow::Diag:
+                reversed.push_back(x[i - 1]);
+                --i;
+                --j;
+                break;
+            case Arrow::Up:
+                --i;
+                break;
+            case Arrow::Left:
+                --j;
+                break;
+        }
+    }
+    return Sequence(std::string(reversed.rbegin(), reversed.rend()));
+}
+
 std::vector<Length> lcs_length_batch(const std::vector<Sequence>& xs,
                                      const std::vector<Sequence>& ys) {
     if (xs.size() != ys.size()) throw std::invalid_argument("lcs_length_batch: size mismatch");

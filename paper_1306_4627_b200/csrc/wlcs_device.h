@@ -97,6 +97,9 @@ cudaError_t pair_split_combine(const uint32_t* vf, const uint32_t* vr, int64_t W
                                uint32_t* scratch, unsigned long long* best, cudaStream_t stream);
 int pair_smem_bytes(int K, int sigma);
 cudaError_t pair_fill(const PairDev& d, int K, bool store, int sms, cudaStream_t stream);
+// The reference's DpTable / BacktrackTable from the stored bit rows.
+cudaError_t pair_tables(const PairDev& d, int K, uint32_t* dp, uint8_t* back,
+                        cudaStream_t stream);
 size_t pair_walk_scratch_bytes(int64_t rows);
 // Exact traceback; out receives the subsequence in FORWARD order.
 cudaError_t pair_walk(const PairDev& d, int K, const uint8_t* x, uint8_t* out,

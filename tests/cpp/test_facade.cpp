@@ -89,6 +89,26 @@ int main() {
     }
     const auto lens = lcs_length_batch(xs, ys);
     for (int k = 0; k < 64; ++k) CHECK(lens[k] == lcs_length(xs[k], ys[k]));
+    // full tables + traceback, as the reference's callers compose them
+    // (test_core.cpp:50-56,74-85: BDAB; serial.hpp:21-30)
+    {
+        const FillResult f = lcs_fill_serial(seq("ABCBDAB"), seq("BDCABA"));
+        CHECK(f.dp.final_length() == 4);
+        CHECK(f.dp.rows() == 8 && f.dp.cols() == 7);
+        CHECK(traceback(f.back, seq("ABCBDAB"), 7, 6) == seq("BDAB"));
+        CHECK(f.back.at(1, 4) == Arrow::Diag);  // x_1 = A == y_4 = A
+        CHECK(throws<std::out_of_range>([&] { traceback(f.back, seq("ABCBDAB"), 8, 6); }));
+        CHECK(throws<CapacityError>([] { lcs_fill_serial(seq("ATGC"), seq("ATGC"), 16); }));
+        const FillResult e = lcs_fill_serial(seq(""), seq("ATGC"));
+        CHECK(e.dp.final_length() == 0 && e.dp.rows() == 1 && e.dp.cols() == 5);
+        std::mt19937_64 rng4(5);
+        for (int k = 0; k < 20; ++k) {
+            const Sequence x = random_dna(rng4, 1 + rng4() % 120), y = random_dna(rng4, 1 + rng4() % 120);
+            const FillResult t = lcs_fill_serial(x, y);
+            CHECK(t.dp.final_length() == lcs_length(x, y));
+            CHECK(traceback(t.back, x, x.size(), y.size()) == lcs_subsequence(x, y));
+        }
+    }
     std::printf("%s (%d failures)\n", failures ? "FAIL" : "PASS", failures);
     return failures;
 }

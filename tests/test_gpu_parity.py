@@ -319,3 +319,39 @@ def test_single_process_multi_gpu_entry_points(wl, restatement):
         wl.lcs_length_batch_multi(xb, xo, yb, yo, n + 1)
     with pytest.raises(wl.ConfigError):
         wl.lcs_length_strips(b"ACGT" * 5000, b"GATTACA" * 5000, n + 1)
+
+
+# ---- the reference's full tables on the device ----
+
+@pytest.mark.parametrize("m,n,alphabet", [(1, 1, DNA), (7, 6, DNA), (37, 129, DNA), (300, 200, PROTEIN),
+                                          (1000, 999, DNA), (64, 2050, PROTEIN)])
+def test_fill_tables_match_oracle(wl, restatement, m, n, alphabet):
+    rng = np.random.default_rng(m + 3 * n)
+    a = np.frombuffer(alphabet, np.uint8)
+    x = a[rng.integers(0, len(a), m)].tobytes()
+    y = a[rng.integers(0, len(a), n)].tobytes()
+    dp, back = wl.fill_tables(x, y)
+    want_dp, want_back = restatement.fill_tables(x, y)
+    assert np.array_equal(dp, want_dp)
+    assert np.array_equal(back, want_back)
+
+
+def test_fill_tables_match_reference_tests(wl, restatement):
+    # acceptance.cpp:101-138 style: 200 seeded small cases, tables identical
+    # to the (restated) serial fill, tracebacks identical
+    rng = np.random.default_rng(2024)
+    for _ in range(200):
+        m, n = int(rng.integers(0, 60)), int(rng.integers(0, 60))
+        x = rng.choice(np.frombuffer(b"AC", np.uint8), m).tobytes()
+        y = rng.choice(np.frombuffer(b"AC", np.uint8), n).tobytes()
+        dp, back = wl.fill_tables(x, y)
+        want_dp, want_back = restatement.fill_tables(x, y)
+        assert np.array_equal(dp, want_dp) and np.array_equal(back, want_back)
+        assert restatement.traceback(back, x, m, n) == wl.lcs_subsequence(x, y)
+
+
+def test_fill_tables_capacity(wl):
+    with pytest.raises(wl.CapacityError):
+        wl.fill_tables(b"ATGC", b"ATGC", 16)
+    dp, back = wl.fill_tables(b"", b"ATGC")
+    assert dp.shape == (1, 5) and not dp.any() and back.shape == (0, 4)
