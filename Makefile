@@ -9,12 +9,13 @@ SRC := paper_1306_4627_b200/csrc
 OBJ := build/obj
 LIB := paper_1306_4627_b200/_lib/libwavelcs_b200.so
 FACADE_TEST := tests/cpp/test_facade
+CLI := paper_1306_4627_b200/_lib/wavelcs_b200
 CU_SRCS := $(wildcard $(SRC)/*.cu)
 CXX_SRCS := $(wildcard $(SRC)/*.cpp)
 OBJS := $(patsubst $(SRC)/%.cu,$(OBJ)/%.o,$(CU_SRCS)) $(patsubst $(SRC)/%.cpp,$(OBJ)/%.cpp.o,$(CXX_SRCS))
 HDRS := $(wildcard $(SRC)/*.cuh) $(wildcard $(SRC)/*.h) $(wildcard include/*.h) $(wildcard include/*.hpp)
 
-all: lib oracle $(FACADE_TEST)
+all: lib oracle $(FACADE_TEST) $(CLI)
 
 lib: $(LIB)
 
@@ -35,6 +36,10 @@ $(FACADE_TEST): tests/cpp/test_facade.cpp $(LIB) include/wavelcs_b200.hpp
 	$(CXX) -std=c++20 -O2 -Wall -Wextra -Iinclude -o $@ $< -L$(dir $(LIB)) -lwavelcs_b200 \
 	    -Wl,-rpath,'$$ORIGIN/../../$(dir $(LIB))'
 
+# Command-line front end on the GPU path (tools/cli).
+$(CLI): tools/cli/wavelcs_b200_main.cpp $(LIB) include/wavelcs_b200.hpp
+	$(CXX) -std=c++20 -O2 -Wall -Wextra -Iinclude -o $@ $< -L$(dir $(LIB)) -lwavelcs_b200 \
+	    -Wl,-rpath,'$$ORIGIN'
 
 $(LIB): $(OBJS)
 	@mkdir -p $(dir $@)
@@ -44,6 +49,6 @@ oracle:
 	$(MAKE) -s -C oracle
 
 clean:
-	rm -rf build $(LIB) $(FACADE_TEST)
+	rm -rf build $(LIB) $(FACADE_TEST) $(CLI)
 
 .PHONY: all lib oracle clean

@@ -18,6 +18,7 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <filesystem>
 #include <stdexcept>
 #include <string>
 #include <string_view>
@@ -150,5 +151,22 @@ std::vector<Length> lcs_length_batch(const std::vector<Sequence>& xs,
                                      const std::vector<Sequence>& ys);
 
 Sequence generate_random(std::size_t length, const Sequence& alphabet, std::uint64_t seed);
+
+/// similarity_percent (sequence.cpp:18-26): 100 * L / |child| (100 when the
+/// child is empty); std::invalid_argument when L > min(M, N).
+double similarity_percent(std::size_t lcs_len, std::size_t parent_len, std::size_t child_len);
+
+// ---- input path (io.hpp / io.cpp semantics) --------
+enum class InputFormat { Plain, Fasta };
+/// ".fa" / ".fasta" -> Fasta, anything else Plain (io.cpp:38-44).
+InputFormat format_from_path(const std::filesystem::path& path) noexcept;
+/// Whole file; Plain strips ASCII whitespace, Fasta keeps the first record
+/// upper-cased; InputError on unreadable files / malformed FASTA; with
+/// validate_dna, InputError on a symbol outside {A,C,G,T} (io.cpp:46-101).
+Sequence load_sequence(const std::filesystem::path& path, InputFormat format,
+                       bool validate_dna = false);
+Sequence parse_fasta(std::string_view bytes);
+void validate_dna_alphabet(const Sequence& seq);
+void write_plain(const Sequence& seq, const std::filesystem::path& path);
 
 }  // namespace wavelcs

@@ -2,6 +2,10 @@
 // C-ABI.  Maps wlcs_status codes back onto the reference's exception types.
 #include "wavelcs_b200.hpp"
 
+#include <algorithm>
+#include <cctype>
+#include <fstream>
+#include <sstream>
 #include <string>
 
 #include "wavelcs_capi.h"
@@ -113,6 +117,88 @@ Sequence generate_random(std::size_t length, const Sequence& alphabet, std::uint
     raise(wlcs_generate_random(length, bytes(alphabet), alphabet.size(), seed,
                                reinterpret_cast<std::uint8_t*>(s.data())));
     return Sequence(std::move(s));
+}
+
+double similarity_percent(std::size_t lcs_len, std::size_t parent_len, std::size_t child_len) {
+    if (lcs_len > std::min(parent_len, child_len))
+        throw std::invalid_argument("similarity_percent: LCS length exceeds min(M, N)");
+    if (child_len == 0) return 100.0;  // empty child fully matches
+    return 100.0 * static_cast<double>(lcs_len) / static_cast<double>(child_len);
+}
+
+namespace {
+bool is_ascii_space(char b) noexcept {
+    return b == ' ' || b == '\t' || b == '\n' || b == '\v' || b == '\f' || b == '\r';
+}
+std::string read_file(const std::filesystem::path& path) {
+    std::ifstream in(path, std::ios::binary);
+    if (!in) throw InputError("cannot open '" + path.string() + "' for reading");
+    std::ostringstream buffer;
+    buffer << in.rdbuf();
+    if (in.bad()) throw InputError("read failure on '" + path.string() + "'");
+    return std::move(buffer).str();
+}
+}  // namespace
+
+InputFormat format_from_path(const std::filesystem::path& path) noexcept {
+    const auto ext = path.extension().string();
+    return (ext == ".fa" || ext == ".fasta") ? InputFormat::Fasta : InputFormat::Plain;
+}
+
+Sequence parse_fasta(std::string_view bytes) {
+    std::string symbols;
+    bool in_record = false;
+    std::size_t pos = 0;
+    while (pos < bytes.size()) {
+        std::size_t eol = bytes.find('\n', pos);
+        if (eol == std::string_view::npos) eol = bytes.size();
+        const std::string_view line = bytes.substr(pos, eol - pos);
+        pos = eol + 1;
+        if (!line.empty() && line.front() == '>') {
+            if (in_record) break;  // first record only
+            in_record = true;
+            continue;
+        }
+        for (const char b : line) {
+            if (is_ascii_space(b)) continue;
+            if (!in_record) throw InputError("malformed FASTA: sequence data before the '>' header");
+            symbols.push_back(static_cast<char>(std::toupper(static_cast<unsigned char>(b))));
+        }
+    }
+    if (!in_record) throw InputError("malformed FASTA: no '>' header found");
+    return Sequence(std::move(symbols));
+}
+
+void validate_dna_alphabet(const Sequence& seq) {
+    for (std::size_t off = 0; off < seq.size(); ++off) {
+        const char b = seq[off];
+        if (!(b == 'A' || b == 'C' || b == 'G' || b == 'T'))
+            throw InputError("symbol '" + std::string(1, b) + "' at offset " + std::to_string(off) +
+                             " is outside the {A, C, G, T} alphabet");
+    }
+}
+
+Sequence load_sequence(const std::filesystem::path& path, InputFormat format, bool validate_dna) {
+    const std::string bytes = read_file(path);
+    Sequence seq;
+    if (format == InputFormat::Fasta) {
+        seq = parse_fasta(bytes);
+    } else {
+        std::string stripped;
+        stripped.reserve(bytes.size());
+        for (const char b : bytes)
+            if (!is_ascii_space(b)) stripped.push_back(b);
+        seq = Sequence(std::move(stripped));
+    }
+    if (validate_dna) validate_dna_alphabet(seq);
+    return seq;
+}
+
+void write_plain(const Sequence& seq, const std::filesystem::path& path) {
+    std::ofstream out(path, std::ios::binary | std::ios::trunc);
+    if (!out) throw InputError("cannot open '" + path.string() + "' for writing");
+    out.write(seq.data(), static_cast<std::streamsize>(seq.size()));
+    if (!out) throw InputError("write failure on '" + path.string() + "'");
 }
 
 }  // namespace wavelcs
