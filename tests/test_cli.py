@@ -87,5 +87,5 @@ def test_bench_csv(tmp_path):
     rc, text = run("bench", "--sizes", "1000x1000,10000x10000", "--repetitions", "2", "--out", str(out))
     assert rc == 0
     rows = [l for l in out.read_text().splitlines() if l and not l.startswith("#")]
-    assert rows[0] == "M,N,repetitions,device_s,gcups,lcs_length"
+    assert rows[0] == "M,N,repetitions,device_s,gcups,roofline_frac,lcs_length"
     assert rows[2].split(",")[-1] == "6538"  # SURVEY 8(c) checkpoint, seed 1

@@ -16,6 +16,7 @@
 #include <vector>
 
 #include "wavelcs_b200.hpp"
+#include "wavelcs_capi.h"
 
 namespace {
 
@@ -111,7 +112,13 @@ int run_bench(Args& a) {
     out << "# wavelcs_b200 benchmark (device: B200, bit-parallel fill)\n";
     out << "# generator: mt19937_64, symbol = alphabet[next() % |alphabet|], alphabet=ACGT\n";
     out << "# seeds: parent = seed, child = seed + 0x9e3779b97f4a7c15\n";
-    out << "M,N,repetitions,device_s,gcups,lcs_length\n";
+    // roofline denominator: the device's measured int32 ALU peak, 3 ops per
+    // 32-cell word-row
+    double peak_ops = 0.0;
+    if (wlcs_probe_int_peak(3, &peak_ops) != WLCS_OK) throw DeviceError(wlcs_last_error());
+    const double gcups_peak = peak_ops * 32.0 / 3.0 / 1e9;
+    out << "# int roofline: " << gcups_peak << " GCUPS (measured int32 ALU peak x 32/3)\n";
+    out << "M,N,repetitions,device_s,gcups,roofline_frac,lcs_length\n";
     size_t n_rec = 0;
     for (const auto& st : sizes) {
         const size_t xpos = st.find_first_of("xX");
@@ -121,6 +128,17 @@ int run_bench(Args& a) {
         const Sequence x = generate_random(m, Sequence("ACGT"), seed);
         const Sequence y = generate_random(n, Sequence("ACGT"), seed + 0x9e3779b97f4a7c15ull);
         Length len = lcs_length(x, y, kNoMemoryBudget);  // warm-up
+        // equivalence gate (bench.cpp:100-106 semantics): the two device
+        // fill variants must agree
+        std::uint32_t wave = 0;
+        if (wlcs_length_ex(reinterpret_cast<const std::uint8_t*>(x.data()), m,
+                           reinterpret_cast<const std::uint8_t*>(y.data()), n, WLCS_NO_BUDGET,
+                           WLCS_VARIANT_WAVEFRONT, &wave) != WLCS_OK)
+            throw DeviceError(wlcs_last_error());
+        if (wave != len)
+            throw EquivalenceError("M=" + std::to_string(m) + " N=" + std::to_string(n) +
+                                   ": bit-parallel " + std::to_string(len) + " vs wavefront " +
+                                   std::to_string(wave));
         double best = 1e300;
         for (unsigned r = 0; r < reps; ++r) {
             const auto t0 = std::chrono::steady_clock::now();
@@ -129,8 +147,9 @@ int run_bench(Args& a) {
                                       std::chrono::steady_clock::now() - t0).count());
         }
         char line[256];
-        std::snprintf(line, sizeof line, "%zu,%zu,%u,%.6f,%.1f,%u\n", m, n, reps, best,
-                      double(m) * double(n) / best / 1e9, len);
+        const double gcups = double(m) * double(n) / best / 1e9;
+        std::snprintf(line, sizeof line, "%zu,%zu,%u,%.6f,%.1f,%.4f,%u\n", m, n, reps, best,
+                      gcups, gcups / gcups_peak, len);
         out << line;
         std::cout << line;
         ++n_rec;
