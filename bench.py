@@ -75,18 +75,25 @@ def parse_args():
 
 # ----------------------------------------------------------------- plumbing
 class Dist:
+    """One process per GPU (torchrun).  NCCL by default; WLCS_DIST_BACKEND=gloo
+    and WLCS_BENCH_ONE_DEVICE=1 exist only to exercise the N > 1 host logic
+    on a single-GPU box (independent shards, no kernel waits on another)."""
+
     def __init__(self):
         self.world = int(os.environ.get("WORLD_SIZE", "1"))
         self.rank = int(os.environ.get("RANK", "0"))
         self.local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+        if os.environ.get("WLCS_BENCH_ONE_DEVICE") == "1":
+            self.local_rank = 0
+        self.backend = os.environ.get("WLCS_DIST_BACKEND", "nccl")
         self.pg = None
 
-    def init(self, backend="nccl"):
+    def init(self):
         import torch
         import torch.distributed as dist
         if self.world > 1 and not dist.is_initialized():
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-            dist.init_process_group(backend)
+            dist.init_process_group(self.backend)
             self.pg = dist
         return self
 
@@ -94,21 +101,18 @@ class Dist:
         if self.pg is not None:
             self.pg.barrier()
 
-    def max(self, v: float) -> float:
-        if self.pg is None:
-            return v
+    def _reduce(self, v: float, op) -> float:
         import torch
-        t = torch.tensor([v], dtype=torch.float64, device="cuda")
-        self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
+        dev = "cuda" if self.backend == "nccl" else "cpu"
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        self.pg.all_reduce(t, op=op)
         return float(t.item())
 
+    def max(self, v: float) -> float:
+        return v if self.pg is None else self._reduce(v, self.pg.ReduceOp.MAX)
+
     def sum(self, v: float) -> float:
-        if self.pg is None:
-            return v
-        import torch
-        t = torch.tensor([v], dtype=torch.float64, device="cuda")
-        self.pg.all_reduce(t, op=self.pg.ReduceOp.SUM)
-        return float(t.item())
+        return v if self.pg is None else self._reduce(v, self.pg.ReduceOp.SUM)
 
 
 class ClockSampler:
@@ -451,7 +455,8 @@ def run_colsplit(args, dist):
                                   in_rev=in_r if g + 1 < G else 0, out_rev=out_r)
         if G == 1:
             return multigpu.colsplit_combine([(lo, hi)], [vf], [vr], len(cols))
-        return multigpu.colsplit_combine_dist(lo, hi, vf, vr, tdist, device=dev)
+        return multigpu.colsplit_combine_dist(lo, hi, vf, vr, tdist,
+                                              device=dev if dist.backend == "nccl" else None)
 
     for _ in range(args.warmup):
         length = step()
