@@ -298,7 +298,7 @@ __global__ void __launch_bounds__(32, 1) pair_strip_kernel(PairDev d) {
         };
         if (feeder) {
             carry_async(0);
-            carry_async(1);
+            if (d.carry_ahead > 1) carry_async(1);
         }
         const uint8_t* pml = pm + lane_off;
         const uint32_t csr = d.code_stride;  // runtime value: address IMAD stays on the FMA pipe
@@ -308,7 +308,8 @@ __global__ void __launch_bounds__(32, 1) pair_strip_kernel(PairDev d) {
         uint32_t cin_lo = 0, cin_hi = 0;
         for (int tg = 0; tg < T; tg += 4) {
             if (feeder && tg < nchunks) {
-                asm volatile("cp.async.wait_group 1;" ::: "memory");  // group tg/4 landed
+                if (d.carry_ahead > 1) asm volatile("cp.async.wait_group 1;" ::: "memory");
+                else asm volatile("cp.async.wait_group 0;" ::: "memory");  // group tg/4 landed
                 __syncwarp();
                 cw = cring[(tg >> 2) & 3];
                 const int lim = nchunks - tg;  // words at or past nchunks stay 0
@@ -317,7 +318,7 @@ __global__ void __launch_bounds__(32, 1) pair_strip_kernel(PairDev d) {
                     cw = carry_ld4(left_carry + tg);  // not yet published: re-poll
                 }
                 __syncwarp();
-                carry_async((tg >> 2) + 2);
+                carry_async((tg >> 2) + d.carry_ahead);
                 prefetch_l2(left_carry + tg + 16);
             }
 #pragma unroll
@@ -758,6 +759,11 @@ cudaError_t pair_code_rows(const uint8_t* row, int64_t rows, bool reverse, const
 template <int K, bool STORE>
 static cudaError_t launch_strip(const PairDev& d, int sms, cudaStream_t stream) {
     const_cast<PairDev&>(d).code_stride = uint32_t(pair_code_stride(K));
+    {
+        const char* ca = std::getenv("WLCS_PAIR_CARRY_AHEAD");
+        const int v = ca && *ca ? std::atoi(ca) : 1;
+        const_cast<PairDev&>(d).carry_ahead = v == 1 ? 1 : 2;
+    }
     const_cast<PairDev&>(d).pm_warp_bytes = uint32_t(d.sigma * pair_code_stride(K));
     const char* env = std::getenv("WLCS_PAIR_WPC");
     int wpc = env && *env ? std::atoi(env) : 1;

@@ -74,6 +74,7 @@ struct PairDev {
     int nprob;
     uint32_t code_stride;   // smem bytes per code record (set by pair_fill)
     uint32_t pm_warp_bytes; // smem bytes of the match masks (set by pair_fill)
+    int carry_ahead;        // carry-word groups staged ahead (1 or 2; set by pair_fill)
     const uint8_t* colp0;   // column string of problem 0 (alphabet scan)
     const uint16_t* map;    // 256 byte -> code map of the column alphabet
     int sigma;              // codes incl. the zero row

@@ -14,3 +14,6 @@ python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/pro
       python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > /dev/null 2>&1
 python tools/launches.py gpurun_out/prof/launches_c2.csv > gpurun_out/prof/launches_c2.txt 2>&1
 cat gpurun_out/prof/pytest_gpu.txt gpurun_out/prof/launches_c2.txt
+# single-pair strip kernel (C4, K=4): one ncu capture after the plain run above
+ncu --set full --import-source on --clock-control none -k regex:pair_strip -c 1 -f -o gpurun_out/prof/c4_strip python bench.py --config c4 --steps 1 --warmup 0 > /dev/null 2>&1
+ls gpurun_out/prof/
