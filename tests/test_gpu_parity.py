@@ -355,3 +355,34 @@ def test_fill_tables_capacity(wl):
         wl.fill_tables(b"ATGC", b"ATGC", 16)
     dp, back = wl.fill_tables(b"", b"ATGC")
     assert dp.shape == (1, 5) and not dp.any() and back.shape == (0, 4)
+
+
+# ---- traceback shapes: skinny tables, far-from-diagonal paths, 256 symbols ----
+
+@pytest.mark.parametrize("m,n", [(1, 50000), (50000, 1), (3, 20000), (20000, 3), (2000, 9000),
+                                 (9000, 2000), (20000, 3000), (257, 255)])
+def test_subsequence_shapes(wl, restatement, m, n):
+    # skinny tables drive the walk's Left runs to column 0 and the
+    # speculative walk's fallback (paths far from the diagonal)
+    rng = np.random.default_rng(m + 31 * n)
+    x = rng.choice(np.frombuffer(DNA, np.uint8), m).tobytes()
+    y = rng.choice(np.frombuffer(DNA, np.uint8), n).tobytes()
+    assert wl.lcs_subsequence(x, y) == restatement.subsequence(x, y)
+
+
+def test_subsequence_byte_alphabet(wl, restatement):
+    rng = np.random.default_rng(256)
+    for m, n in [(3000, 2500), (700, 4000), (4000, 700)]:
+        x = rng.integers(0, 256, m).astype(np.uint8).tobytes()
+        y = rng.integers(0, 256, n).astype(np.uint8).tobytes()
+        assert wl.lcs_length(x, y) == restatement.length_bitpar(x, y)
+        assert wl.lcs_subsequence(x, y) == restatement.subsequence(x, y)
+
+
+def test_subsequence_similar_strings(wl, restatement):
+    # C3-like: a mutated copy keeps the path near the diagonal; shifted copies
+    # move it far off the diagonal (the walk's window must follow)
+    from paper_1306_4627_b200 import workloads
+    x = restatement.generate_random(12000, DNA, 77)
+    for y in (workloads.mutate(x, 5), x[3000:] + x[:3000], b"ACGT" * 500 + x):
+        assert wl.lcs_subsequence(x, y) == restatement.subsequence(x, y)
