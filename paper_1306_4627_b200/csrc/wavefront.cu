@@ -3,8 +3,9 @@
 // Same integer result as the bit-parallel variant and as the reference's
 // cell recurrence (proj/src/serial.cpp:16-30, cell.hpp:20-38):
 //   c[i][j] = x_i == y_j ? c[i-1][j-1] + 1 : max(c[i-1][j], c[i][j-1])
-// evaluated branch-free with the Hopper/Blackwell DPX instructions as
-//   c = __viaddmax_s32(diag, match, max(up, left))
+// evaluated branch-free with the Blackwell DPX three-way max as
+//   c = __vimax3_s32(up, left, diag + match)
+// (diag + match is one add-with-carry of the row's match bit)
 // (valid because c[i-1][j-1] + 1 >= max(up, left) on a match and
 // c[i-1][j-1] <= max(up, left) always).
 //
@@ -37,9 +38,6 @@ constexpr int kWaveBand = 32 * kWaveR;
 constexpr int kWaveWarps = 4;       // warps per CTA (batch kernel)
 constexpr int kWaveTab = 32 * 256;     // per-warp match table bytes: [lane][byte] -> R-bit row mask
 
-__device__ __forceinline__ int32_t cell(int32_t diag, int32_t up, int32_t left, int32_t match) {
-    return __viaddmax_s32(diag, match, max(up, left));
-}
 
 // Steps of one band: lane l owns rows i0 + R l + r.  Prov(t, up, y) is
 // called by the whole warp at step t and sets, for lane 0 (column t), the top
@@ -51,7 +49,7 @@ __device__ __forceinline__ int32_t sweep_band(const uint8_t* rowp, int64_t i0, i
                                               int64_t n, uint8_t* tab, Prov prov,
                                               BottomFn bottom, int64_t want_row) {
     const int lane = int(lane_id());
-    // lane's match table: tab[lane][c] bit r = (x_{i0 + R lane + r} == c)
+    // lane's match table: tab[lane][c] bit 7-r = (x_{i0 + R lane + r} == c)
     uint8_t* mt = tab + lane * 256;
     __syncwarp();
 #pragma unroll
@@ -59,7 +57,7 @@ __device__ __forceinline__ int32_t sweep_band(const uint8_t* rowp, int64_t i0, i
 #pragma unroll
     for (int r = 0; r < kWaveR; ++r) {
         const int64_t i = i0 + int64_t(lane) * kWaveR + r;
-        if (i < m) mt[rowp[i]] |= uint8_t(1u << r);
+        if (i < m) mt[rowp[i]] |= uint8_t(0x80u >> r);  // row r at bit 7 - r
     }
     __syncwarp();
     int32_t left[kWaveR];
@@ -77,11 +75,17 @@ __device__ __forceinline__ int32_t sweep_band(const uint8_t* rowp, int64_t i0, i
         const int32_t up = lane == 0 ? up0 : int32_t(recv >> 8);
         const uint32_t y = lane == 0 ? y0 : (recv & 0xffu);
         if (j >= 0 && j < n) {
-            const uint32_t mrow = mt[y];
+            // row r's match bit at bit 31 - r: each row shifts it into the
+            // carry flag, and diag + match is one add-with-carry
+            uint32_t mm = uint32_t(mt[y]) << 24;
             int32_t u = up, dg = prev_up;
 #pragma unroll
             for (int r = 0; r < kWaveR; ++r) {
-                const int32_t v = cell(dg, u, left[r], int32_t((mrow >> r) & 1u));
+                int32_t dm;
+                asm("{\n\tadd.cc.u32 %0, %0, %0;\n\taddc.u32 %1, %2, 0;\n\t}"
+                    : "+r"(mm), "=r"(dm)
+                    : "r"(dg));
+                const int32_t v = __vimax3_s32(u, left[r], dm);
                 dg = left[r];
                 left[r] = v;
                 u = v;
