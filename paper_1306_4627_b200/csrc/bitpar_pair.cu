@@ -158,7 +158,6 @@ __device__ __forceinline__ void st_relaxed_sys_nb(uint32_t* p, uint32_t v) {
 }
 
 constexpr uint32_t kCarryValid = 0x10000u;  // carry words: valid flag | 16-row mask
-constexpr int kPairWarps = 1;               // warps per CTA (one strip per warp; more only shares sub-partitions)
 
 // Row coding: entry i = map[row byte i] (the row's match-mask record in the
 // strip's shared-memory table is at code * code_stride).  Rows
@@ -211,7 +210,8 @@ __global__ void pair_code_rows_kernel(const uint8_t* row, int64_t rows, int reve
 // shuffles per step (rows 0-7 after row 7, rows 8-15 after row 15), so the
 // shuffle latency hides behind row work.
 //
-// Launch: 1-warp CTAs (one strip each), up to the occupancy limit.
+// Launch: 1-warp CTAs (one strip each), up to the occupancy limit (more
+// warps per CTA were measured: no gain, strips only share sub-partitions).
 template <int K, bool STORE>
 __global__ void __launch_bounds__(32, 1) pair_strip_kernel(PairDev d) {
     extern __shared__ __align__(16) uint8_t smem[];
@@ -739,14 +739,8 @@ int64_t pair_code_plane(int nchunks) { return int64_t(nchunks) + 2 * kPadChunks;
 cudaError_t pair_code_rows(const uint8_t* row, int64_t rows, bool reverse, const uint16_t* map,
                            int K, FillProblem& P, uint4* coded_base, cudaStream_t stream) {
     const int64_t nchp = pair_code_plane(P.nchunks);
-    const char* env = std::getenv("WLCS_PAIR_LAYOUT");
-    if (env && *env == '1') {  // chunk-contiguous
-        P.plane = 1;
-        P.cstride = 4;
-    } else {  // planes
-        P.plane = nchp;
-        P.cstride = 1;
-    }
+    P.plane = nchp;  // 4 planes of uint4, one uint4 per chunk and plane
+    P.cstride = 1;
     P.coded = coded_base + kPadChunks * P.cstride;
     const int64_t total = nchp * 16;
     const int64_t b = (total + 255) / 256;
@@ -757,33 +751,24 @@ cudaError_t pair_code_rows(const uint8_t* row, int64_t rows, bool reverse, const
 }
 
 template <int K, bool STORE>
-static cudaError_t launch_strip(const PairDev& d, int sms, cudaStream_t stream) {
-    const_cast<PairDev&>(d).code_stride = uint32_t(pair_code_stride(K));
-    {
-        const char* ca = std::getenv("WLCS_PAIR_CARRY_AHEAD");
-        const int v = ca && *ca ? std::atoi(ca) : 1;
-        const_cast<PairDev&>(d).carry_ahead = v == 1 ? 1 : 2;
-    }
-    const_cast<PairDev&>(d).pm_warp_bytes = uint32_t(d.sigma * pair_code_stride(K));
-    const char* env = std::getenv("WLCS_PAIR_WPC");
-    int wpc = env && *env ? std::atoi(env) : 1;
-    if (wpc < 1 || wpc > kPairWarps) wpc = 1;
-    int smem = wpc * pair_smem_bytes(K, d.sigma);
-    const char* solo = std::getenv("WLCS_PAIR_SOLO");
-    if (solo && *solo == '1' && smem < 116 * 1024) smem = 116 * 1024;  // one CTA per SM
+static cudaError_t launch_strip(const PairDev& dev, int sms, cudaStream_t stream) {
+    PairDev d = dev;
+    d.code_stride = uint32_t(pair_code_stride(K));
+    d.pm_warp_bytes = uint32_t(d.sigma * pair_code_stride(K));
+    d.carry_ahead = 1;  // carry-word groups staged ahead (2 measured slower)
+    const int smem = pair_smem_bytes(K, d.sigma);
     cudaError_t e = cudaFuncSetAttribute(pair_strip_kernel<K, STORE>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     int occ = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pair_strip_kernel<K, STORE>, 32 * wpc,
-                                                      smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pair_strip_kernel<K, STORE>, 32, smem);
     if (e != cudaSuccess) return e;
     if (occ < 1) occ = 1;
     const int strips = d.nprob * d.prob[0].nstrips;
-    int grid = (strips + wpc - 1) / wpc;
+    int grid = strips;
     if (grid > sms * occ) grid = sms * occ;
-    if (grid * 32 * wpc > kPairSinkWords) grid = kPairSinkWords / (32 * wpc);
-    pair_strip_kernel<K, STORE><<<grid, 32 * wpc, smem, stream>>>(d);
+    if (grid * 32 > kPairSinkWords) grid = kPairSinkWords / 32;
+    pair_strip_kernel<K, STORE><<<grid, 32, smem, stream>>>(d);
     return cudaGetLastError();
 }
 
