@@ -205,22 +205,44 @@ struct TaskInfo {
     uint32_t first, last;
 };
 
-__device__ __forceinline__ TaskInfo decode_task(const BatchDev& d, uint32_t t, uint32_t lane) {
+// The task table (per class order: task start, pair start, pair count) is
+// constant during the sweep kernel: every lane keeps orders `lane` and
+// `lane + 32` in registers, so decoding a task is ballots and shuffles only.
+struct TaskTable {
+    uint32_t ts0, ts1, ps0, ps1, cn0, cn1;
+};
+
+__device__ __forceinline__ TaskTable load_task_table(const BatchDev& d, uint32_t lane) {
     const uint32_t* count = d.meta + kMetaCount;
     const uint32_t* pair_start = d.meta + kMetaPairStart;
     const uint32_t* task_start = d.meta + kMetaTaskStart;
-    const bool le0 = task_start[lane] <= t;
-    const bool le1 = lane + 32 < kNumClasses && task_start[lane + 32] <= t;
-    const int order = __popc(__ballot_sync(kFullMask, le0)) +
-                      __popc(__ballot_sync(kFullMask, le1)) - 1;
+    const bool hi = lane + 32 < kNumClasses;
+    TaskTable tt;
+    tt.ts0 = task_start[lane];
+    tt.ps0 = pair_start[lane];
+    tt.cn0 = count[lane];
+    tt.ts1 = hi ? task_start[lane + 32] : 0xffffffffu;
+    tt.ps1 = hi ? pair_start[lane + 32] : 0u;
+    tt.cn1 = hi ? count[lane + 32] : 0u;
+    return tt;
+}
+
+__device__ __forceinline__ TaskInfo decode_task(const TaskTable& tt, uint32_t t) {
+    const int order = __popc(__ballot_sync(kFullMask, tt.ts0 <= t)) +
+                      __popc(__ballot_sync(kFullMask, tt.ts1 <= t)) - 1;
+    const int src = order & 31;
+    const bool up = order >= 32;
+    const uint32_t ts = __shfl_sync(kFullMask, up ? tt.ts1 : tt.ts0, src);
+    const uint32_t ps = __shfl_sync(kFullMask, up ? tt.ps1 : tt.ps0, src);
+    const uint32_t cn = __shfl_sync(kFullMask, up ? tt.cn1 : tt.cn0, src);
     const int c = kNumClasses - 1 - order;
     TaskInfo ti;
     ti.sidx = c / kMaxK;
     ti.K = c % kMaxK + 1;
     ti.S = 1 << ti.sidx;
     const uint32_t per_task = 32u >> ti.sidx;
-    ti.first = pair_start[order] + (t - task_start[order]) * per_task;
-    const uint32_t end = pair_start[order] + count[order];
+    ti.first = ps + (t - ts) * per_task;
+    const uint32_t end = ps + cn;
     ti.last = ti.first + per_task < end ? ti.first + per_task : end;
     return ti;
 }
@@ -488,12 +510,13 @@ __global__ void __launch_bounds__(32) batch_main_kernel(BatchDev d) {
     extern __shared__ __align__(16) uint8_t smem[];  // map [256] | inv [256] | PM
     const uint32_t lane = lane_id();
     const uint32_t total = d.meta[kMetaTaskStart + kNumClasses];
+    const TaskTable tt = load_task_table(d, lane);
     for (;;) {
         uint32_t t = 0;
         if (lane == 0) t = atomicAdd(d.meta + kMetaCounter, 1u);
         t = __shfl_sync(kFullMask, t, 0);
         if (t >= total) break;
-        const TaskInfo ti = decode_task(d, t, lane);
+        const TaskInfo ti = decode_task(tt, t);
         const int K = ti.K;
         const int S = ti.S;
         const int s = int(lane) & (S - 1);
