@@ -386,3 +386,20 @@ def test_subsequence_similar_strings(wl, restatement):
     x = restatement.generate_random(12000, DNA, 77)
     for y in (workloads.mutate(x, 5), x[3000:] + x[:3000], b"ACGT" * 500 + x):
         assert wl.lcs_subsequence(x, y) == restatement.subsequence(x, y)
+
+
+@pytest.mark.parametrize("name", ["c4", "c5"])
+def test_large_configs_golden(wl, name):
+    """Full-size C4 / C5 lengths equal the CPU oracle's (tests/golden/
+    large_configs.json, made by tests/golden/make_large_golden.py); both
+    fill variants and the in-order column split."""
+    import json
+    import os
+    from paper_1306_4627_b200 import workloads
+    with open(os.path.join(os.path.dirname(__file__), "golden", "large_configs.json")) as f:
+        want = json.load(f)[name]["lcs_length"]
+    x, y = workloads.config_pair(name)
+    assert wl.lcs_length(x, y, wl.NO_BUDGET) == want
+    assert wl.lcs_length(x, y, wl.NO_BUDGET, variant=wl.VARIANT_WAVEFRONT) == want
+    if name == "c4":
+        assert _colsplit_in_order(wl, x, y, 2) == want
