@@ -254,7 +254,7 @@ def run_reference_arm(args, dist):
     line = {
         "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * total / args.steps, 3),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8/u32",
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
         "data": "synthetic", "impl": "reference",
         "config": {"workload": "C2: 65536 protein-like pairs, 20 letters, lengths U[200,1000]",
                    "global_batch": args.pairs, "seq_len": "200-1000", "parallelism": "cpu-threads"},
@@ -361,7 +361,7 @@ def run_c2(args, dist):
         "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": dist.world,
         "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(total_ms / args.steps, 4), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "u32 (bit-vector words), u8 symbols",
+        "scaling": "weak", "vs_baseline": None, "dtype": "u32",
         "data": "synthetic (seeded std::mt19937_64, wlcs_generate_pairs)",
         "config": {"workload": "C2: 65536 protein-like pairs per GPU, 20-letter alphabet, "
                                "lengths U[200,1000], LCS length per pair",
