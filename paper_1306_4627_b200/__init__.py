@@ -185,10 +185,16 @@ def pack_pairs(xs: _Seq, ys: _Seq):
     return xbuf, xoff, ybuf, yoff
 
 
+def _as_u8(a) -> np.ndarray:
+    if isinstance(a, (bytes, bytearray, memoryview)):
+        return np.frombuffer(a, dtype=np.uint8)
+    return np.ascontiguousarray(a, dtype=np.uint8)
+
+
 def lcs_length_batch(xs, x_off, ys, y_off, variant: int = VARIANT_BITPARALLEL) -> np.ndarray:
-    """Lengths of many independent pairs (host arrays)."""
-    xs = np.ascontiguousarray(xs, dtype=np.uint8)
-    ys = np.ascontiguousarray(ys, dtype=np.uint8)
+    """Lengths of many independent pairs (host arrays or bytes)."""
+    xs = _as_u8(xs)
+    ys = _as_u8(ys)
     x_off = np.ascontiguousarray(x_off, dtype=np.uint64)
     y_off = np.ascontiguousarray(y_off, dtype=np.uint64)
     pairs = len(x_off) - 1
@@ -278,10 +284,8 @@ def colsplit_fill(x, y, col_lo: int, col_hi: int, problems: int = 3, in_fwd: int
 
 def lcs_length_batch_multi(xs, x_off, ys, y_off, n_gpus: int) -> np.ndarray:
     """Batch sharded over devices 0..n_gpus-1 of this process."""
-    xs = np.ascontiguousarray(np.frombuffer(xs, np.uint8) if isinstance(xs, (bytes, bytearray))
-                              else xs, np.uint8)
-    ys = np.ascontiguousarray(np.frombuffer(ys, np.uint8) if isinstance(ys, (bytes, bytearray))
-                              else ys, np.uint8)
+    xs = _as_u8(xs)
+    ys = _as_u8(ys)
     x_off = np.ascontiguousarray(x_off, np.uint64)
     y_off = np.ascontiguousarray(y_off, np.uint64)
     pairs = len(x_off) - 1

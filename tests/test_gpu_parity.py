@@ -403,3 +403,20 @@ def test_large_configs_golden(wl, name):
     assert wl.lcs_length(x, y, wl.NO_BUDGET, variant=wl.VARIANT_WAVEFRONT) == want
     if name == "c4":
         assert _colsplit_in_order(wl, x, y, 2) == want
+
+
+def test_batch_many_tiny_pairs(wl, restatement):
+    # 200k pairs of 0..40 symbols: exercises the plan/scan/scatter at scale and
+    # the empty-pair early outs (proj/tests/test_parallel.cpp:236-242)
+    rng = np.random.default_rng(11)
+    pairs = 200_000
+    lm = rng.integers(0, 41, pairs)
+    ln = rng.integers(0, 41, pairs)
+    a = np.frombuffer(DNA, np.uint8)
+    xb = a[rng.integers(0, 4, int(lm.sum()))].tobytes()
+    yb = a[rng.integers(0, 4, int(ln.sum()))].tobytes()
+    xo = np.concatenate([[0], np.cumsum(lm)]).astype(np.uint64)
+    yo = np.concatenate([[0], np.cumsum(ln)]).astype(np.uint64)
+    got = wl.lcs_length_batch(xb, xo, yb, yo)
+    want = restatement.length_batch(np.frombuffer(xb, np.uint8), xo, np.frombuffer(yb, np.uint8), yo)
+    assert np.array_equal(got, want)
