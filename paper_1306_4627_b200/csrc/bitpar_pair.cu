@@ -403,13 +403,17 @@ __global__ void __launch_bounds__(32, 1) pair_strip_kernel(PairDev d) {
 //  2. resolve (one thread, bottom block first): the true entry of block k is
 //     the exit of block k-1; if it lies between two candidates whose walks
 //     left the block at the same column, that column is the exit (O(1)),
-//     otherwise the block is walked from the true entry (rare);
+//     otherwise the block is walked from the true entry until the walk meets
+//     a neighbouring candidate's column recorded every kWalkCkpt rows (rare,
+//     and short: adjacent walks merge within a few dozen rows);
 //  3. emit: every block is walked again, in parallel, from its true entry,
 //     flagging the rows that emit;
 //  4. the flagged row bytes are compacted in row order (forward string).
 constexpr int kWalkRows = 256;
 constexpr int kWalkCand = 128;   // candidates per block (4 warps)
 constexpr int kWalkStride = 16;  // columns between candidates
+constexpr int kWalkCkpt = 32;    // rows between recorded candidate columns
+constexpr int kWalkNCkpt = kWalkRows / kWalkCkpt;
 
 template <int K>
 __device__ __forceinline__ uint32_t walk_code(const FillProblem& P, int64_t q) {
@@ -452,7 +456,8 @@ __device__ __forceinline__ int64_t walk_cand(int64_t guess, int l, int64_t N) {
 
 // 1. one CTA (kWalkCand threads) per block of rows
 template <int K>
-__global__ void __launch_bounds__(kWalkCand) walk_spec_kernel(PairDev d, int32_t* exits) {
+__global__ void __launch_bounds__(kWalkCand) walk_spec_kernel(PairDev d, int32_t* exits,
+                                                              int32_t* ckpt) {
     __shared__ uint32_t codes[kWalkRows];
     const FillProblem& P = d.prob[0];
     const int64_t M = P.rows, N = P.cols;
@@ -463,17 +468,20 @@ __global__ void __launch_bounds__(kWalkCand) walk_spec_kernel(PairDev d, int32_t
         codes[top - i] = walk_code<K>(P, i - 1);
     __syncthreads();
     int64_t j = walk_cand(walk_guess(top, M, N), int(threadIdx.x), N);
-    for (int64_t i = top; i > lo && j > 0; --i) {
+    int32_t* ck = ckpt + k * (kWalkNCkpt * kWalkCand) + threadIdx.x;
+    for (int64_t i = top; i > lo; --i) {
         uint32_t dg;
-        j = walk_step<K>(P, codes[top - i], i - 1, j, &dg);
+        if (j > 0) j = walk_step<K>(P, codes[top - i], i - 1, j, &dg);
+        const int64_t done = top - i + 1;  // rows walked so far
+        if (done % kWalkCkpt == 0 && done < kWalkRows) ck[(done / kWalkCkpt) * kWalkCand] = int32_t(j);
     }
     exits[k * kWalkCand + threadIdx.x] = int32_t(j);
 }
 
 // 2. one thread; entry[k] = true entry column of block k
 template <int K>
-__global__ void walk_resolve_kernel(PairDev d, const int32_t* exits, int32_t* entry,
-                                    uint32_t* misses) {
+__global__ void walk_resolve_kernel(PairDev d, const int32_t* exits, const int32_t* ckpt,
+                                    int32_t* entry, uint32_t* misses) {
     const FillProblem& P = d.prob[0];
     const int64_t M = P.rows, N = P.cols;
     const int64_t nb = (M + kWalkRows - 1) / kWalkRows;
@@ -496,13 +504,31 @@ __global__ void walk_resolve_kernel(PairDev d, const int32_t* exits, int32_t* en
                      ex[l] == ex[l + 1])
                 next = ex[l];
         }
-        if (next < 0) {  // outside the window or the bracket did not merge
+        if (next < 0) {
+            // Outside the window or the bracket had not merged at the block's
+            // end: walk from the true entry, but stop at the first checkpoint
+            // where the walk meets a candidate's recorded column (from there
+            // on it IS that candidate's path).
             ++miss;
-            next = j;
-            for (int64_t i = top; i > lo && next > 0; --i) {
+            const int32_t* ck = ckpt + k * (kWalkNCkpt * kWalkCand);
+            int64_t lb = l0 < 0 ? 0 : (l0 >= kWalkCand ? kWalkCand - 1 : l0);
+            int64_t jw = j;
+            for (int64_t i = top; i > lo; --i) {
                 uint32_t dg;
-                next = walk_step<K>(P, walk_code<K>(P, i - 1), i - 1, next, &dg);
+                if (jw > 0) jw = walk_step<K>(P, walk_code<K>(P, i - 1), i - 1, jw, &dg);
+                const int64_t done = top - i + 1;
+                if (done % kWalkCkpt == 0 && done < kWalkRows) {
+                    const int32_t* row = ck + (done / kWalkCkpt) * kWalkCand;
+                    int64_t hit = -1;
+                    for (int64_t l = lb - 1; l <= lb + 1 && hit < 0; ++l)
+                        if (l >= 0 && l < kWalkCand && row[l] == jw) hit = l;
+                    if (hit >= 0) {
+                        next = ex[hit];
+                        break;
+                    }
+                }
             }
+            if (next < 0) next = jw;
         }
         j = next;
     }
@@ -788,7 +814,7 @@ cudaError_t pair_fill(const PairDev& d, int K, bool store, int sms, cudaStream_t
 
 size_t pair_walk_scratch_bytes(int64_t rows) {
     const int64_t nb = (rows + kWalkRows - 1) / kWalkRows;
-    return size_t(nb) * kWalkCand * 4 + size_t(nb) * 12 + size_t(rows) + 64;
+    return size_t(nb) * kWalkCand * 4 * (1 + kWalkNCkpt) + size_t(nb) * 12 + size_t(rows) + 64;
 }
 
 cudaError_t pair_walk(const PairDev& d, int K, const uint8_t* x, uint8_t* out,
@@ -797,15 +823,16 @@ cudaError_t pair_walk(const PairDev& d, int K, const uint8_t* x, uint8_t* out,
     const int64_t M = d.prob[0].rows;
     const int64_t nb = (M + kWalkRows - 1) / kWalkRows;
     int32_t* exits = static_cast<int32_t*>(scratch);
-    int32_t* entry = exits + nb * kWalkCand;
+    int32_t* ckpt = exits + nb * kWalkCand;
+    int32_t* entry = ckpt + nb * kWalkCand * kWalkNCkpt;
     uint32_t* counts = reinterpret_cast<uint32_t*>(entry + nb);
     uint32_t* offsets = counts + nb;
     uint8_t* flags = reinterpret_cast<uint8_t*>(offsets + nb);
     const int tb = 128;
     const int eb = int((nb + tb - 1) / tb);
     auto run = [&](auto spec, auto resolve, auto emit) {
-        spec<<<int(nb), kWalkCand, 0, stream>>>(d, exits);
-        resolve<<<1, 1, 0, stream>>>(d, exits, entry, misses);
+        spec<<<int(nb), kWalkCand, 0, stream>>>(d, exits, ckpt);
+        resolve<<<1, 1, 0, stream>>>(d, exits, ckpt, entry, misses);
         emit<<<eb, tb, 0, stream>>>(d, entry, flags, counts);
         walk_scan_kernel<<<1, 1, 0, stream>>>(counts, nb, offsets, out_len);
         walk_write_kernel<<<eb, tb, 0, stream>>>(x, M, flags, offsets, out);
