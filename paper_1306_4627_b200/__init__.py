@@ -37,7 +37,7 @@ __all__ = [
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_lib", "libwavelcs_b200.so")
+LIB_PATH = os.environ.get("WLCS_LIB_PATH") or os.path.join(HERE, "_lib", "libwavelcs_b200.so")
 
 DEFAULT_MEMORY_BUDGET = 2 * 1024 ** 3  # kDefaultMemoryBudget, include/wavelcs/tables.hpp:12
 NO_BUDGET = 2 ** 64 - 1

@@ -10,7 +10,7 @@
 //  * plan:   one thread per pair picks the roles (the shorter string becomes
 //            the bit-vector "column" string -- LCS length is symmetric,
 //            SPEC.md:82), its word count W = ceil(cols/32) and a lane shape
-//            (S lanes per pair, K <= 8 words per lane, S*K >= W).  A counting
+//            (S lanes per pair, K <= 12 words per lane, S*K >= W).  A counting
 //            sort (plan -> scan -> scatter) groups pairs by shape and, inside
 //            a shape, by decreasing 16-row chunk count, so the pairs of one
 //            warp task end on the same step.
@@ -32,8 +32,12 @@
 namespace wlcs {
 namespace {
 
-constexpr int kMaxK = 8;
-constexpr int kNumClasses = 6 * kMaxK;   // S in {1,2,4,8,16,32} x K in 1..8
+constexpr int kMaxK = 12;
+#ifndef WLCS_BATCH_HALF_UNROLL
+#define WLCS_BATCH_HALF_UNROLL 1
+#endif
+constexpr int kHalfUnroll = WLCS_BATCH_HALF_UNROLL;  // half-chunk loop unroll (1: smaller code)
+constexpr int kNumClasses = 6 * kMaxK;   // S in {1,2,4,8,16,32} x K in 1..12
 constexpr int kChunkBuckets = 128;       // chunk-count buckets per class (clamped)
 constexpr int kBuckets = kNumClasses * kChunkBuckets;
 constexpr int kMapBytes = 512;  // map [256] + inverse code list [256]
@@ -64,9 +68,10 @@ __global__ void __launch_bounds__(256) batch_plan_kernel(BatchDev d, uint32_t* h
     __shared__ uint32_t local[kBuckets];
     for (int i = threadIdx.x; i < kBuckets; i += blockDim.x) local[i] = 0;
     __syncthreads();
-    const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t p = i < d.pairs ? (d.ids ? d.ids[i] : i) : 0u;
     uint32_t b = kNoBucket, r = 0;
-    if (p < d.pairs) {
+    if (i < d.pairs) {
         const uint64_t m = d.xoff[p + 1] - d.xoff[p];
         const uint64_t n = d.yoff[p + 1] - d.yoff[p];
         const uint64_t cols = m < n ? m : n;
@@ -99,9 +104,9 @@ __global__ void __launch_bounds__(256) batch_plan_kernel(BatchDev d, uint32_t* h
         if (c) local[i] = atomicAdd(hist + i, c);  // block base inside bucket i
     }
     __syncthreads();
-    if (p < d.pairs) {
-        bucket[p] = b;
-        rank[p] = b == kNoBucket ? 0u : local[b] + r;
+    if (i < d.pairs) {
+        bucket[i] = b;
+        rank[i] = b == kNoBucket ? 0u : local[b] + r;
     }
 }
 
@@ -166,11 +171,11 @@ __global__ void __launch_bounds__(1024) batch_scan_kernel(BatchDev d, const uint
 __global__ void __launch_bounds__(256) batch_scatter_kernel(BatchDev d, const uint32_t* bucket,
                                                             const uint32_t* rank,
                                                             const uint32_t* start) {
-    const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= d.pairs) return;
-    const uint32_t b = bucket[p];
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= d.pairs) return;
+    const uint32_t b = bucket[i];
     if (b == kNoBucket) return;
-    d.vals[start[b] + rank[p]] = p;
+    d.vals[start[b] + rank[i]] = d.ids ? d.ids[i] : i;
 }
 
 // Per-lane view of its pair inside a task.
@@ -178,7 +183,7 @@ struct LanePair {
     const uint8_t* colp;  // column (bit-vector) string = the shorter one
     const uint8_t* rowp;
     const uint8_t *col_lo, *col_hi, *row_lo, *row_hi;
-    int cols;             // <= 8192 in the batch path
+    int cols;             // <= 12288 in the batch path
     int64_t rows;
 };
 
@@ -206,35 +211,40 @@ struct TaskInfo {
 };
 
 // The task table (per class order: task start, pair start, pair count) is
-// constant during the sweep kernel: every lane keeps orders `lane` and
-// `lane + 32` in registers, so decoding a task is ballots and shuffles only.
+// constant during the sweep kernel: every lane keeps orders `lane`,
+// `lane + 32` and `lane + 64` in registers, so decoding a task is ballots and
+// shuffles only.
+constexpr int kTableSlots = (kNumClasses + 31) / 32;
+static_assert(kTableSlots == 3, "task table slots");
 struct TaskTable {
-    uint32_t ts0, ts1, ps0, ps1, cn0, cn1;
+    uint32_t ts[kTableSlots], ps[kTableSlots], cn[kTableSlots];
 };
 
 __device__ __forceinline__ TaskTable load_task_table(const BatchDev& d, uint32_t lane) {
     const uint32_t* count = d.meta + kMetaCount;
     const uint32_t* pair_start = d.meta + kMetaPairStart;
     const uint32_t* task_start = d.meta + kMetaTaskStart;
-    const bool hi = lane + 32 < kNumClasses;
     TaskTable tt;
-    tt.ts0 = task_start[lane];
-    tt.ps0 = pair_start[lane];
-    tt.cn0 = count[lane];
-    tt.ts1 = hi ? task_start[lane + 32] : 0xffffffffu;
-    tt.ps1 = hi ? pair_start[lane + 32] : 0u;
-    tt.cn1 = hi ? count[lane + 32] : 0u;
+#pragma unroll
+    for (int i = 0; i < kTableSlots; ++i) {
+        const uint32_t o = lane + 32u * i;
+        const bool ok = o < uint32_t(kNumClasses);
+        tt.ts[i] = ok ? task_start[o] : 0xffffffffu;
+        tt.ps[i] = ok ? pair_start[o] : 0u;
+        tt.cn[i] = ok ? count[o] : 0u;
+    }
     return tt;
 }
 
 __device__ __forceinline__ TaskInfo decode_task(const TaskTable& tt, uint32_t t) {
-    const int order = __popc(__ballot_sync(kFullMask, tt.ts0 <= t)) +
-                      __popc(__ballot_sync(kFullMask, tt.ts1 <= t)) - 1;
+    int order = -1;
+#pragma unroll
+    for (int i = 0; i < kTableSlots; ++i) order += __popc(__ballot_sync(kFullMask, tt.ts[i] <= t));
     const int src = order & 31;
-    const bool up = order >= 32;
-    const uint32_t ts = __shfl_sync(kFullMask, up ? tt.ts1 : tt.ts0, src);
-    const uint32_t ps = __shfl_sync(kFullMask, up ? tt.ps1 : tt.ps0, src);
-    const uint32_t cn = __shfl_sync(kFullMask, up ? tt.cn1 : tt.cn0, src);
+    const int slot = order >> 5;
+    const uint32_t ts = __shfl_sync(kFullMask, slot == 0 ? tt.ts[0] : slot == 1 ? tt.ts[1] : tt.ts[2], src);
+    const uint32_t ps = __shfl_sync(kFullMask, slot == 0 ? tt.ps[0] : slot == 1 ? tt.ps[1] : tt.ps[2], src);
+    const uint32_t cn = __shfl_sync(kFullMask, slot == 0 ? tt.cn[0] : slot == 1 ? tt.cn[1] : tt.cn[2], src);
     const int c = kNumClasses - 1 - order;
     TaskInfo ti;
     ti.sidx = c / kMaxK;
@@ -309,22 +319,21 @@ __device__ __forceinline__ void word_bytes(const uint4& c0, const uint4& c1, con
 // the warp's shared-memory slice; *zrep receives a byte value absent from the
 // alphabet, replicated x4 (used to blank invalid rows in the sweep).
 __device__ __forceinline__ uint32_t build_task(const BatchDev& d, const LanePair& p, int K, int s,
-                                            uint8_t* smem, uint32_t* zrep) {
+                                            uint32_t sbase, uint32_t* zrep) {
     const uint32_t lane = lane_id();
-    uint8_t* map = smem;         // byte -> code
-    uint8_t* inv = smem + 256;   // u16 low-nibble presence per high nibble
-    uint8_t* pm = smem + kMapBytes;
+    const uint32_t map = sbase;         // byte -> code
+    const uint32_t inv = sbase + 256u;  // u16 low-nibble presence per high nibble
+    const uint32_t pm = sbase + uint32_t(kMapBytes);
     const bool wide = K > 4;
-    const uint32_t cs = wide ? 1024u : 128u * uint32_t(K == 3 ? 4 : K);
+    const uint32_t cs = wide ? 512u * uint32_t((K + 3) / 4) : 128u * uint32_t(K == 3 ? 4 : K);
     const uint32_t ls = wide ? 16u : 4u * uint32_t(K == 3 ? 4 : K);
 
     // presence flags: one 32-bit word per byte value in the (not yet used) PM
     // region -- lanes marking the same byte hit the same word (no conflict)
-    uint32_t* flags = reinterpret_cast<uint32_t*>(pm);
+    const uint32_t flags = pm;
     __syncwarp();
 #pragma unroll
-    for (int i = 0; i < 2; ++i)
-        reinterpret_cast<uint4*>(flags)[lane * 2 + i] = make_uint4(0u, 0u, 0u, 0u);
+    for (int i = 0; i < 2; ++i) sts_v4(flags + 16u * (lane * 2 + i), make_uint4(0u, 0u, 0u, 0u));
 
     // The lane's columns [c0, c0 + clen), read as the 16-byte aligned chunks
     // 0..2K of the region starting a_c bytes before them.
@@ -352,7 +361,7 @@ __device__ __forceinline__ uint32_t build_task(const BatchDev& d, const LanePair
             const int nv = min(max(clen - 32 * k, 0), 32);
 #pragma unroll
             for (int j = 0; j < 32; ++j)
-                if (j < nv) flags[__byte_perm(w[j >> 2], 0u, 0x4440u | uint32_t(j & 3))] = 1u;
+                if (j < nv) sts_u32(flags + 4u * __byte_perm(w[j >> 2], 0u, 0x4440u | uint32_t(j & 3)), 1u);
             c0v = c2v;
             c1v = n1;
             c2v = n2;
@@ -365,8 +374,8 @@ __device__ __forceinline__ uint32_t build_task(const BatchDev& d, const LanePair
     uint32_t sigma, hm = 0;
     uint32_t* hmask = &hm;
     {
-        const uint4 f0 = reinterpret_cast<const uint4*>(flags)[lane * 2];
-        const uint4 f1 = reinterpret_cast<const uint4*>(flags)[lane * 2 + 1];
+        const uint4 f0 = lds_v4(flags + 32u * lane);
+        const uint4 f1 = lds_v4<16>(flags + 32u * lane);
         const uint32_t present = (f0.x ? 1u : 0u) | (f0.y ? 2u : 0u) | (f0.z ? 4u : 0u) |
                                  (f0.w ? 8u : 0u) | (f1.x ? 16u : 0u) | (f1.y ? 32u : 0u) |
                                  (f1.z ? 64u : 0u) | (f1.w ? 128u : 0u);  // byte 8*lane + b
@@ -399,8 +408,8 @@ __device__ __forceinline__ uint32_t build_task(const BatchDev& d, const LanePair
             __shfl_sync(kFullMask, uint32_t(8 * lane) + __ffs(absent) - 1, __ffs(has) - 1);
         *zrep = zb * 0x01010101u;
         __syncwarp();
-        reinterpret_cast<uint2*>(map)[lane] = make_uint2(ox, oy);
-        if ((lane & 1u) == 0u) reinterpret_cast<uint16_t*>(inv)[lane >> 1] = uint16_t(nib16);
+        sts_v2(map + 8u * lane, ox, oy);
+        if ((lane & 1u) == 0u) sts_u16(inv + lane, nib16);
     }
     __syncwarp();
 
@@ -419,7 +428,7 @@ __device__ __forceinline__ uint32_t build_task(const BatchDev& d, const LanePair
             const uint32_t vmask = nv >= 32 ? 0xffffffffu : ((1u << nv) - 1u);
             const uint32_t woff =
                 lane_off + (wide ? uint32_t((k >> 2) * 512 + (k & 3) * 4) : uint32_t(k * 4));
-            *reinterpret_cast<uint32_t*>(pm + woff) = 0u;  // code 0: the zero row
+            sts_u32(pm + woff, 0u);  // code 0: the zero row
             // match mask of byte v = h*16 + 4j + i:
             //   hi(h) & b[j] & a[i],  a[i] / b[j] = equality masks of the bit
             //   pairs (planes 0,1) / (planes 2,3), hi(h) = planes 4..7 == h
@@ -432,8 +441,8 @@ __device__ __forceinline__ uint32_t build_task(const BatchDev& d, const LanePair
                 const uint32_t hi_acc =
                     vmask & ~((P[4] ^ (0u - (h & 1u))) | (P[5] ^ (0u - ((h >> 1) & 1u))) |
                               (P[6] ^ (0u - ((h >> 2) & 1u))) | (P[7] ^ (0u - ((h >> 3) & 1u))));
-                const uint32_t nm = reinterpret_cast<const uint16_t*>(inv)[h];
-                const uint8_t* mrow = map + h * 16u;
+                const uint32_t nm = lds_u16(inv + 2u * h);
+                const uint32_t mrow = map + h * 16u;
 #pragma unroll
                 for (int jj = 0; jj < 4; ++jj) {
                     if ((nm >> (4 * jj)) & 0xfu) {
@@ -441,8 +450,8 @@ __device__ __forceinline__ uint32_t build_task(const BatchDev& d, const LanePair
 #pragma unroll
                         for (int ii = 0; ii < 4; ++ii) {
                             if ((nm >> (4 * jj + ii)) & 1u) {
-                                const uint32_t c = mrow[4 * jj + ii];
-                                *reinterpret_cast<uint32_t*>(pm + c * cs + woff) = hb & a[ii];
+                                const uint32_t c = lds_u8(mrow + uint32_t(4 * jj + ii));
+                                sts_u32(pm + c * cs + woff, hb & a[ii]);
                             }
                         }
                     }
@@ -454,14 +463,20 @@ __device__ __forceinline__ uint32_t build_task(const BatchDev& d, const LanePair
         }
     }
     __syncwarp();
+    // the inverse table is done: zero it for the sweep (the all-zero map of
+    // chunks outside a row string)
+    sts_v2(inv + 8u * lane, 0u, 0u);
+    __syncwarp();
     return sigma;
 }
 
 // Row sweep of a task whose masks are built.  S (lanes per pair) is runtime;
 // returns the lane's count of zero bits below `cols`.
+// Generic form: 64-bit chunk bounds and allocation checks every step (tasks
+// whose row strings touch the ends of the input buffers).
 template <bool CHAIN, int K>
-__device__ __forceinline__ int sweep_task(const BatchDev& d, const LanePair& p, int S, int s,
-                                       const uint8_t* smem, uint32_t zrep) {
+__device__ __noinline__ int sweep_task_generic(const BatchDev& d, const LanePair& p, int S, int s,
+                                               const uint8_t* smem, uint32_t zrep) {
     const uint32_t lane = lane_id();
     const uint8_t* map = smem;
     const uint8_t* pm = smem + kMapBytes;
@@ -501,9 +516,67 @@ __device__ __forceinline__ int sweep_task(const BatchDev& d, const LanePair& p, 
     return lane_zero_count<K>(V, int64_t(s) * K, p.cols);
 }
 
+// Fast form (every lane's chunks lie inside its buffer): per step one
+// 16-byte load of the next chunk, 32-bit chunk classification, and the
+// byte -> code table switched to the all-zero table for chunks outside the
+// row string (identity rows); only the two partial chunks of a row string
+// are sanitized.  Shared memory is addressed through one 32-bit base.
+template <bool CHAIN, int K>
+__device__ __forceinline__ int sweep_task(const BatchDev& d, const LanePair& p, int S, int s,
+                                          const uint8_t* smem, uint32_t sbase, uint32_t zrep) {
+    const int a_r = int(reinterpret_cast<uintptr_t>(p.rowp) & 15u);
+    const uint8_t* rstart = p.rowp - a_r;
+    const int rows = int(p.rows);  // < 2^30 in the batch path
+    const int nrch = rows > 0 ? (rows + a_r + 15) >> 4 : 0;
+    const bool inb =
+        nrch == 0 || (rstart >= p.row_lo && rstart + 16 * int64_t(nrch) <= p.row_hi);
+    if (!__all_sync(kFullMask, inb)) return sweep_task_generic<CHAIN, K>(d, p, S, s, smem, zrep);
+    const uint32_t lane = lane_id();
+    const uint32_t map_a = sbase;
+    const uint32_t zmap_a = map_a + 256u;  // zeroed after the build: every byte -> code 0
+    const uint32_t pm_a = map_a + uint32_t(kMapBytes) + PmLayout<K>::word_offset(lane, 0);
+    uint32_t V[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) V[k] = 0xffffffffu;
+    const int T = warp_max(nrch) + S - 1;
+    uint32_t cout = 0;
+    int lo = -16 * s - a_r;  // row index of byte 0 of chunk ch = t - s
+    const uint4* cptr = reinterpret_cast<const uint4*>(rstart);
+    uint4 cur = __ldg((s == 0 && nrch > 0) ? cptr : d.safe16);
+    const uint4* nptr = cptr + (1 - s);  // chunk ch + 1
+    for (int t = 0; t < T; ++t) {
+        const int ch = t - s;
+        const bool nv = unsigned(ch + 1) < unsigned(nrch);
+        const uint4 nxt = __ldg(nv ? nptr : d.safe16);
+        ++nptr;
+        uint32_t cin = 0;
+        if constexpr (CHAIN) {
+            cin = __shfl_up_sync(kFullMask, cout, 1, S);
+            if (s == 0) cin = 0;
+            cin <<= 16;
+            cout = 0;
+        }
+        const bool none = lo >= rows || lo <= -16;
+        const bool part = !none && (lo < 0 || lo > rows - 16);
+        if (__any_sync(kFullMask, part)) {
+            if (part) cur = sanitize_chunk(cur, valid_mask16(lo, rows), zrep);
+        }
+        const uint32_t ma = none ? zmap_a : map_a;
+#pragma unroll kHalfUnroll
+        for (int h = 0; h < 2; ++h) {
+            const uint32_t wlo = h ? cur.z : cur.x;
+            const uint32_t whi = h ? cur.w : cur.y;
+            rows8_sh<CHAIN, K>(V, ma, pm_a, wlo, whi, cin, cout);
+        }
+        cur = nxt;
+        lo += 16;
+    }
+    return lane_zero_count<K>(V, int64_t(s) * K, p.cols);
+}
+
 #define WLCS_SWEEP_CASE(CH, KK) \
-    case (CH) * 8 + (KK - 1):   \
-        zeros = sweep_task<CH, KK>(d, p, S, s, smem, zrep); \
+    case (CH) * 16 + (KK - 1):  \
+        zeros = sweep_task<CH, KK>(d, p, S, s, smem, sbase, zrep); \
         break;
 
 __global__ void __launch_bounds__(32) batch_main_kernel(BatchDev d) {
@@ -511,6 +584,10 @@ __global__ void __launch_bounds__(32) batch_main_kernel(BatchDev d) {
     const uint32_t lane = lane_id();
     const uint32_t total = d.meta[kMetaTaskStart + kNumClasses];
     const TaskTable tt = load_task_table(d, lane);
+    // shared base address, computed once (opaque, so it is not re-derived
+    // from SR_CgaCtaId inside the loops)
+    uint32_t sbase;
+    asm volatile("mov.b32 %0, %1;" : "=r"(sbase) : "r"(smem_u32(smem)));
     for (;;) {
         uint32_t t = 0;
         if (lane == 0) t = atomicAdd(d.meta + kMetaCounter, 1u);
@@ -525,19 +602,21 @@ __global__ void __launch_bounds__(32) batch_main_kernel(BatchDev d) {
         const uint32_t pair = active ? d.vals[idx] : 0u;
         const LanePair p = lane_pair(d, active, pair);
         uint32_t zrep = 0;
-        if (build_task(d, p, K, s, smem, &zrep) == 0u) {
+        if (build_task(d, p, K, s, sbase, &zrep) == 0u) {
             // Alphabet too large for this warp's shared-memory slice.
             if (active && s == 0) d.overflow[atomicAdd(d.meta + kMetaOverflow, 1u)] = pair;
             continue;
         }
         int zeros = 0;
-        switch ((S > 1 ? 8 : 0) + (K - 1)) {
+        switch ((S > 1 ? 16 : 0) + (K - 1)) {
             WLCS_SWEEP_CASE(0, 1) WLCS_SWEEP_CASE(0, 2) WLCS_SWEEP_CASE(0, 3)
             WLCS_SWEEP_CASE(0, 4) WLCS_SWEEP_CASE(0, 5) WLCS_SWEEP_CASE(0, 6)
-            WLCS_SWEEP_CASE(0, 7) WLCS_SWEEP_CASE(0, 8)
+            WLCS_SWEEP_CASE(0, 7) WLCS_SWEEP_CASE(0, 8) WLCS_SWEEP_CASE(0, 9)
+            WLCS_SWEEP_CASE(0, 10) WLCS_SWEEP_CASE(0, 11) WLCS_SWEEP_CASE(0, 12)
             WLCS_SWEEP_CASE(1, 1) WLCS_SWEEP_CASE(1, 2) WLCS_SWEEP_CASE(1, 3)
             WLCS_SWEEP_CASE(1, 4) WLCS_SWEEP_CASE(1, 5) WLCS_SWEEP_CASE(1, 6)
-            WLCS_SWEEP_CASE(1, 7) WLCS_SWEEP_CASE(1, 8)
+            WLCS_SWEEP_CASE(1, 7) WLCS_SWEEP_CASE(1, 8) WLCS_SWEEP_CASE(1, 9)
+            WLCS_SWEEP_CASE(1, 10) WLCS_SWEEP_CASE(1, 11) WLCS_SWEEP_CASE(1, 12)
             default:
                 break;  // unreachable
         }

@@ -85,7 +85,7 @@ struct Ctx {
     cudaStream_t copy_stream = nullptr;  // host batch pipeline: H2D of chunk k+1 || compute of k
     std::vector<cudaEvent_t> chunk_ev;
     // batch
-    DevBuf xs, ys, xoff, yoff, out, ws;
+    DevBuf xs, ys, xoff, yoff, out, ws, ws2;
     // single pair
     DevBuf px, py, pmg, carry, small, rows, outrev, codes, ry, vbuf, wave, sink, walk;
     ~Ctx() {
@@ -168,8 +168,8 @@ struct PairPlan {
 // pipeline + hand-off); strips beyond the resident warps run in waves; more
 // resident strips than sub-partitions share issue slots.
 int batch_kmax() {
-    const int k = env_int("WLCS_BATCH_KMAX", 8);
-    return k >= 1 && k <= 8 ? k : 8;
+    const int k = env_int("WLCS_BATCH_KMAX", 12);
+    return k >= 1 && k <= 12 ? k : 12;
 }
 
 int choose_k(const Ctx& c, int64_t W, int64_t rows_per_prob, int sigma, int nprob) {
@@ -386,6 +386,33 @@ int pair_length_variant(Ctx& c, const uint8_t* dx, size_t m, const uint8_t* dy, 
 }
 
 // ------------------------------------------------------------------ batch
+// Second batch pass over the pairs the first pass could not take because
+// their column alphabet did not fit the warp's mask budget: one word per lane
+// (128-byte code rows, so every byte alphabet fits in 257 * 128 bytes).
+// `d` describes the first pass (its offsets / outputs); `list` is its device
+// overflow list of n entries.  Pairs still left (wider than 32 words, or all
+// 256 byte values present) are returned in `left` for the strip kernel.
+int batch_overflow_pass(Ctx& c, wlcs::BatchDev d, const uint32_t* list, uint32_t n,
+                        cudaStream_t s, std::vector<uint32_t>& left) {
+    left.clear();
+    if (n == 0) return WLCS_OK;
+    d.ids = list;
+    d.pairs = n;
+    d.kmax = 1;
+    d.pm_bytes = 257 * 128;
+    WLCS_CUDA(c.ws2.ensure(wlcs::batch_workspace_bytes(n, d.pm_bytes)));
+    WLCS_CUDA(wlcs::batch_launch(d, c.ws2.p, c.sms, s));
+    uint32_t n2 = 0;
+    WLCS_CUDA(cudaMemcpyAsync(&n2, wlcs::batch_overflow_count_ptr(c.ws2.p, n), 4,
+                              cudaMemcpyDeviceToHost, s));
+    WLCS_CUDA(cudaStreamSynchronize(s));
+    if (n2 == 0) return WLCS_OK;
+    left.resize(n2);
+    WLCS_CUDA(cudaMemcpy(left.data(), wlcs::batch_overflow_list_ptr(c.ws2.p, n), n2 * 4,
+                         cudaMemcpyDeviceToHost));
+    return WLCS_OK;
+}
+
 int batch_device(Ctx& c, const uint8_t* d_xs, const uint64_t* d_xoff, const uint8_t* d_ys,
                  const uint64_t* d_yoff, size_t pairs, uint64_t xs_bytes, uint64_t ys_bytes,
                  int variant, uint32_t* d_out, cudaStream_t stream) {
@@ -432,7 +459,7 @@ int batch_device(Ctx& c, const uint8_t* d_xs, const uint64_t* d_xoff, const uint
         }
         return WLCS_OK;
     }
-    const int pm_bytes = env_int("WLCS_BATCH_PM_KB", 24) * 1024;
+    const int pm_bytes = env_int("WLCS_BATCH_PM_KB", 33) * 1024;
     const size_t ws_bytes = wlcs::batch_workspace_bytes(uint32_t(pairs), pm_bytes);
     WLCS_CUDA(c.ws.ensure(ws_bytes));
     wlcs::BatchDev d{};
@@ -459,10 +486,12 @@ int batch_device(Ctx& c, const uint8_t* d_xs, const uint64_t* d_xoff, const uint
     WLCS_CUDA(cudaStreamSynchronize(stream));
     if (c.timing) WLCS_CUDA(cudaEventElapsedTime(&c.last_main_ms, c.ev0, c.ev1));
     if (overflow == 0) return WLCS_OK;
-    // Pairs too long or with too large an alphabet for one warp: strip kernel.
-    std::vector<uint32_t> ids(overflow);
-    WLCS_CUDA(cudaMemcpy(ids.data(), wlcs::batch_overflow_list_ptr(c.ws.p, uint32_t(pairs)),
-                         overflow * 4, cudaMemcpyDeviceToHost));
+    // Alphabet too large for the lane shape: second pass at one word per lane;
+    // pairs too long for one warp: strip kernel.
+    std::vector<uint32_t> ids;
+    if (int rc = batch_overflow_pass(c, d, wlcs::batch_overflow_list_ptr(c.ws.p, uint32_t(pairs)),
+                                     overflow, stream, ids))
+        return rc;
     for (uint32_t p : ids) {
         uint64_t xo[2], yo[2];
         WLCS_CUDA(cudaMemcpy(xo, d_xoff + p, 16, cudaMemcpyDeviceToHost));
@@ -490,7 +519,7 @@ int batch_host_pipelined(Ctx& c, const uint8_t* xs, const uint64_t* x_off, const
         WLCS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         c.chunk_ev.push_back(e);
     }
-    const int pm_bytes = env_int("WLCS_BATCH_PM_KB", 24) * 1024;
+    const int pm_bytes = env_int("WLCS_BATCH_PM_KB", 33) * 1024;
     std::vector<size_t> p0(nchunks + 1);
     for (int k = 0; k <= nchunks; ++k) p0[k] = pairs * size_t(k) / size_t(nchunks);
     std::vector<size_t> ws_off(nchunks + 1, 0);
@@ -539,14 +568,30 @@ int batch_host_pipelined(Ctx& c, const uint8_t* xs, const uint64_t* x_off, const
                                   4, cudaMemcpyDeviceToHost, s));
     WLCS_CUDA(cudaStreamSynchronize(s));
     if (c.timing) WLCS_CUDA(cudaEventElapsedTime(&c.last_main_ms, c.ev0, c.ev1));
+    std::vector<std::vector<uint32_t>> left(nchunks);
+    bool second = false;
     for (int k = 0; k < nchunks; ++k) {
         if (!ovf[k]) continue;
-        std::vector<uint32_t> ids(ovf[k]);
-        WLCS_CUDA(cudaMemcpy(ids.data(),
-                             wlcs::batch_overflow_list_ptr(c.ws.as<uint8_t>() + ws_off[k],
-                                                           uint32_t(p0[k + 1] - p0[k])),
-                             ovf[k] * 4, cudaMemcpyDeviceToHost));
-        for (uint32_t q : ids) {
+        wlcs::BatchDev d{};
+        d.xs = dxs;
+        d.xoff = c.xoff.as<uint64_t>() + p0[k];
+        d.xs_bytes = xs_bytes;
+        d.ys = dys;
+        d.yoff = c.yoff.as<uint64_t>() + p0[k];
+        d.ys_bytes = ys_bytes;
+        d.out = c.out.as<uint32_t>() + p0[k];
+        if (int rc = batch_overflow_pass(
+                c, d,
+                wlcs::batch_overflow_list_ptr(c.ws.as<uint8_t>() + ws_off[k],
+                                              uint32_t(p0[k + 1] - p0[k])),
+                ovf[k], s, left[k]))
+            return rc;
+        second = true;
+    }
+    if (second)
+        WLCS_CUDA(cudaMemcpy(out, c.out.p, pairs * 4, cudaMemcpyDeviceToHost));
+    for (int k = 0; k < nchunks; ++k) {
+        for (uint32_t q : left[k]) {
             const size_t p = p0[k] + q;
             uint32_t len = 0;
             int rc = pair_length_device(c, dxs + x_off[p], size_t(x_off[p + 1] - x_off[p]),

@@ -8,8 +8,8 @@
 //   V    = row update          (rowstep.cuh: AND, IADD3.X, LOP3 per word)
 // Shared-memory match-mask layout, chosen so every warp-wide PM load is
 // bank-conflict free:
-//   K <= 4 : [code][lane][K words]             code stride 128*K bytes
-//   K  > 4 : [code][K/4 slot][lane][4 words]   code stride 1024 bytes
+//   K <= 4 : [code][lane][K words]               code stride 128*K bytes
+//   K  > 4 : [code][ceil(K/4) slot][lane][4 words] code stride 512*ceil(K/4)
 #pragma once
 
 #include "rowstep.cuh"
@@ -20,7 +20,8 @@ namespace wlcs {
 template <int K>
 struct PmLayout {
     static constexpr int kWide = K > 4;
-    static constexpr uint32_t code_stride = kWide ? 1024u : 128u * uint32_t(K == 3 ? 4 : K);
+    static constexpr uint32_t code_stride =
+        kWide ? 512u * uint32_t((K + 3) / 4) : 128u * uint32_t(K == 3 ? 4 : K);
     static constexpr uint32_t lane_stride = kWide ? 16u : 4u * uint32_t(K == 3 ? 4 : K);
     // byte offset of word k of `lane` inside one code row
     __device__ __forceinline__ static uint32_t word_offset(uint32_t lane, int k) {
@@ -29,20 +30,24 @@ struct PmLayout {
     }
 };
 
+// Slot i (words 4i .. 4i+3) of a wide row sits at byte offset 512*i.
 template <int K>
 __device__ __forceinline__ void load_pm(const uint8_t* pm, uint32_t off, uint32_t* P) {
     if constexpr (K >= 4) {
-        const uint4 a = *reinterpret_cast<const uint4*>(pm + off);
-        P[0] = a.x; P[1] = a.y; P[2] = a.z; P[3] = a.w;
-        if constexpr (K == 8 || K == 7) {
-            const uint4 b = *reinterpret_cast<const uint4*>(pm + off + 512);
-            P[4] = b.x; P[5] = b.y; P[6] = b.z;
-            if constexpr (K == 8) P[7] = b.w;
-        } else if constexpr (K == 6) {
-            const uint2 b = *reinterpret_cast<const uint2*>(pm + off + 512);
-            P[4] = b.x; P[5] = b.y;
-        } else if constexpr (K == 5) {
-            P[4] = *reinterpret_cast<const uint32_t*>(pm + off + 512);
+#pragma unroll
+        for (int i = 0; 4 * i < K; ++i) {
+            const uint8_t* q = pm + off + 512 * i;
+            const int n = K - 4 * i < 4 ? K - 4 * i : 4;
+            if (n == 4) {
+                const uint4 a = *reinterpret_cast<const uint4*>(q);
+                P[4 * i] = a.x; P[4 * i + 1] = a.y; P[4 * i + 2] = a.z; P[4 * i + 3] = a.w;
+            } else if (n >= 2) {
+                const uint2 a = *reinterpret_cast<const uint2*>(q);
+                P[4 * i] = a.x; P[4 * i + 1] = a.y;
+                if (n == 3) P[4 * i + 2] = *reinterpret_cast<const uint32_t*>(q + 8);
+            } else {
+                P[4 * i] = *reinterpret_cast<const uint32_t*>(q);
+            }
         }
     } else if constexpr (K == 3) {
         const uint2 a = *reinterpret_cast<const uint2*>(pm + off);
@@ -152,6 +157,118 @@ __device__ __forceinline__ uint4 fetch_chunk(const uint8_t* rstart, int ch, uint
         if (slow) c = load_chunk16(p, alloc_lo, alloc_hi);
     }
     return c;
+}
+
+// ---------------------------------------------------------------------------
+// Explicit 32-bit shared-memory addressing.  With generic pointers into the
+// dynamic shared window the compiler re-derives the window base
+// (S2R SR_CgaCtaId + LEA) inside loops; these keep one base in a register.
+// The asm is volatile so loads stay ordered after the stores / __syncwarp()
+// of the mask build.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ uint32_t lds_u8(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ uint32_t lds_u16(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u16 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+template <int OFF = 0>
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1+%2];" : "=r"(v) : "r"(a), "n"(OFF));
+    return v;
+}
+template <int OFF = 0>
+__device__ __forceinline__ uint2 lds_v2(uint32_t a) {
+    uint2 v;
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2+%3];" : "=r"(v.x), "=r"(v.y) : "r"(a), "n"(OFF));
+    return v;
+}
+template <int OFF = 0>
+__device__ __forceinline__ uint4 lds_v4(uint32_t a) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4+%5];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "r"(a), "n"(OFF));
+    return v;
+}
+__device__ __forceinline__ void sts_u32(uint32_t a, uint32_t v) {
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void sts_u16(uint32_t a, uint32_t v) {
+    asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"(uint16_t(v)) : "memory");
+}
+__device__ __forceinline__ void sts_v2(uint32_t a, uint32_t x, uint32_t y) {
+    asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(a), "r"(x), "r"(y) : "memory");
+}
+__device__ __forceinline__ void sts_v4(uint32_t a, uint4 v) {
+    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v.x), "r"(v.y),
+                 "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+
+// load_pm over a 32-bit shared address (same layouts as load_pm).
+template <int K, int I>
+__device__ __forceinline__ void load_slot_sh(uint32_t a, uint32_t* P) {
+    constexpr int n = K - 4 * I < 4 ? K - 4 * I : 4;
+    if constexpr (n == 4) {
+        const uint4 x = lds_v4<512 * I>(a);
+        P[4 * I] = x.x; P[4 * I + 1] = x.y; P[4 * I + 2] = x.z; P[4 * I + 3] = x.w;
+    } else if constexpr (n >= 2) {
+        const uint2 x = lds_v2<512 * I>(a);
+        P[4 * I] = x.x; P[4 * I + 1] = x.y;
+        if constexpr (n == 3) P[4 * I + 2] = lds_u32<512 * I + 8>(a);
+    } else {
+        P[4 * I] = lds_u32<512 * I>(a);
+    }
+}
+
+// load_pm over a 32-bit shared address (same layouts as load_pm).
+template <int K>
+__device__ __forceinline__ void load_pm_sh(uint32_t a, uint32_t* P) {
+    if constexpr (K >= 4) {
+        load_slot_sh<K, 0>(a, P);
+        if constexpr (K > 4) load_slot_sh<K, 1>(a, P);
+        if constexpr (K > 8) load_slot_sh<K, 2>(a, P);
+    } else if constexpr (K == 3) {
+        const uint2 x = lds_v2(a);
+        P[0] = x.x; P[1] = x.y;
+        P[2] = lds_u32<8>(a);
+    } else if constexpr (K == 2) {
+        const uint2 x = lds_v2(a);
+        P[0] = x.x; P[1] = x.y;
+    } else {
+        P[0] = lds_u32(a);
+    }
+}
+
+// rows8 over shared addresses: map_a = byte -> code table, pm_a = this
+// lane's word 0 of code 0.
+template <bool CHAIN, int K>
+__device__ __forceinline__ void rows8_sh(uint32_t* V, uint32_t map_a, uint32_t pm_a, uint32_t lo,
+                                         uint32_t hi, uint32_t& cin, uint32_t& cout) {
+    constexpr uint32_t cs = PmLayout<K>::code_stride;
+    uint32_t off[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+        off[r] = lds_u8(map_a + __byte_perm(r < 4 ? lo : hi, 0u, 0x4440u | uint32_t(r & 3))) * cs +
+                 pm_a;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+        uint32_t P[K];
+        load_pm_sh<K>(off[r], P);
+        if constexpr (CHAIN) {
+            RowStep<K>::chain(V, P, cin, cout);
+        } else {
+            RowStep<K>::plain(V, P);
+        }
+    }
 }
 
 // Zero bits of the lane's K words below global column `cols`; `word0` is the

@@ -17,9 +17,10 @@ struct BatchDev {
     const uint64_t* yoff;
     uint64_t ys_bytes;
     uint32_t* out;         // pairs lengths
-    uint32_t pairs;
+    uint32_t pairs;        // entries to process (of ids when set)
+    const uint32_t* ids;   // optional: entry i is pair ids[i] (nullptr: pair i)
     int pm_bytes;          // shared-memory bytes for match masks per warp
-    int kmax;              // largest words-per-lane K of a lane shape (<= 8)
+    int kmax;              // largest words-per-lane K of a lane shape (<= 12)
     // filled by batch_launch from the workspace
     uint32_t* keys_in;
     uint32_t* vals_in;

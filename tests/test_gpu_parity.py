@@ -76,6 +76,34 @@ def test_batch_edges(wl, restatement):
     check_batch(wl, restatement, xs, ys)
 
 
+def test_batch_large_alphabet_many(wl, restatement):
+    """Thousands of 256-symbol pairs: their alphabets overflow the first
+    pass's mask budget and take the one-word-per-lane second pass (columns
+    <= 1024) or the strip kernel (wider); also through the device entry point."""
+    import torch
+    rng = np.random.default_rng(99)
+    a = np.arange(256, dtype=np.uint8)
+    xs, ys = [], []
+    for _ in range(3000):
+        m, n = int(rng.integers(1, 1400)), int(rng.integers(1, 1400))
+        xs.append(a[rng.integers(0, 256, m)].tobytes())
+        ys.append(a[np.minimum(rng.zipf(1.3, n), 256) - 1].tobytes())
+    check_batch(wl, restatement, xs, ys)
+    xb, xo, yb, yo = wl.pack_pairs(xs, ys)
+    dev = torch.device("cuda", 0)
+    d_xs = torch.from_numpy(np.concatenate([xb, np.zeros(16, np.uint8)])).to(dev)
+    d_ys = torch.from_numpy(np.concatenate([yb, np.zeros(16, np.uint8)])).to(dev)
+    d_xo = torch.from_numpy(xo.view(np.int64)).to(dev)
+    d_yo = torch.from_numpy(yo.view(np.int64)).to(dev)
+    d_out = torch.zeros(len(xs), dtype=torch.int32, device=dev)
+    wl.lcs_length_batch_device(d_xs.data_ptr(), d_xo.data_ptr(), d_ys.data_ptr(), d_yo.data_ptr(),
+                               len(xs), int(xo[-1]), int(yo[-1]), d_out.data_ptr(),
+                               torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert np.array_equal(d_out.cpu().numpy().astype(np.uint32),
+                          restatement.length_batch(xb, xo, yb, yo))
+
+
 @pytest.mark.parametrize("m,n", [(1, 1), (5, 300), (300, 5), (1000, 1000), (4097, 33), (33, 4097),
                                  (5000, 200), (12345, 6789)])
 def test_single_pair_lengths(wl, restatement, m, n):
