@@ -348,14 +348,48 @@ __device__ __forceinline__ uint32_t build_task(const BatchDev& d, const LanePair
         const uint32_t vm = i <= 2 * K ? valid_mask16(16 * i - a_c, clen) : 0u;
         return fetch_chunk(cstart, i, vm, p.col_lo, p.col_hi, d.safe16);
     };
-    __syncwarp();  // flags zeroed
-
-    // pass 1: mark the bytes present (next word's chunks prefetched)
+    // Stage the lane's 2K+1 column chunks in shared memory with cp.async
+    // (one exposed global latency per task instead of one per word and pass):
+    // at the end of the mask region, [chunk][lane] x 16 bytes.  Pass 2 reads
+    // the stage only when the task's masks do not reach it.
+    const int nchk = 2 * K + 1;
+    const uint32_t stage = pm + uint32_t(d.pm_bytes) - uint32_t(nchk) * 512u;
     {
-        uint4 c0v = chunk(0), c1v = chunk(1), c2v = chunk(2);
+        bool slow = false;
+        for (int i = 0; i < nchk; ++i) {
+            const uint8_t* src = cstart + 16 * i;
+            const uint32_t vm = valid_mask16(16 * i - a_c, clen);
+            const bool inb = src >= p.col_lo && src + 16 <= p.col_hi;
+            slow |= vm != 0u && !inb;
+            const void* g = (vm != 0u && inb) ? static_cast<const void*>(src)
+                                                : static_cast<const void*>(d.safe16);
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(stage + uint32_t(i) * 512u +
+                                                                           lane * 16u),
+                         "l"(g)
+                         : "memory");
+        }
+        asm volatile("cp.async.commit_group;\n\tcp.async.wait_all;" ::: "memory");
+        if (__any_sync(kFullMask, slow)) {  // a chunk straddles the buffer end (rare)
+            for (int i = 0; i < nchk; ++i) {
+                const uint8_t* src = cstart + 16 * i;
+                const uint32_t vm = valid_mask16(16 * i - a_c, clen);
+                if (vm != 0u && !(src >= p.col_lo && src + 16 <= p.col_hi))
+                    sts_v4(stage + uint32_t(i) * 512u + lane * 16u,
+                           load_chunk16(src, p.col_lo, p.col_hi));
+            }
+        }
+    }
+    auto staged = [&](int i) {
+        return i < nchk ? lds_v4(stage + uint32_t(i) * 512u + lane * 16u) : make_uint4(0u, 0u, 0u, 0u);
+    };
+    __syncwarp();  // flags zeroed, stage filled
+
+    // pass 1: mark the bytes present
+    {
+        uint4 c0v = staged(0), c1v = staged(1), c2v = staged(2);
 #pragma unroll 1
         for (int k = 0; k < K; ++k) {
-            const uint4 n1 = chunk(2 * k + 3), n2 = chunk(2 * k + 4);
+            const uint4 n1 = staged(2 * k + 3), n2 = staged(2 * k + 4);
             uint32_t w[8];
             word_bytes(c0v, c1v, c2v, q, fs, w);
             const int nv = min(max(clen - 32 * k, 0), 32);
@@ -416,11 +450,13 @@ __device__ __forceinline__ uint32_t build_task(const BatchDev& d, const LanePair
     // pass 2, word by word: bit-planes, then every code's match mask
     // = valid columns whose byte equals the code's byte value.
     const uint32_t lane_off = wide ? lane * 16u : lane * ls;
+    const bool use_stage = sigma * cs <= uint32_t(d.pm_bytes) - uint32_t(nchk) * 512u;
+    auto chunk2 = [&](int i) { return use_stage ? staged(i) : chunk(i); };
     {
-        uint4 c0v = chunk(0), c1v = chunk(1), c2v = chunk(2);
+        uint4 c0v = chunk2(0), c1v = chunk2(1), c2v = chunk2(2);
 #pragma unroll 1
         for (int k = 0; k < K; ++k) {
-            const uint4 n1 = chunk(2 * k + 3), n2 = chunk(2 * k + 4);
+            const uint4 n1 = chunk2(2 * k + 3), n2 = chunk2(2 * k + 4);
             uint32_t w[8], P[8];
             word_bytes(c0v, c1v, c2v, q, fs, w);
             bit_planes(w, P);

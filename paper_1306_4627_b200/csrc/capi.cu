@@ -459,7 +459,7 @@ int batch_device(Ctx& c, const uint8_t* d_xs, const uint64_t* d_xoff, const uint
         }
         return WLCS_OK;
     }
-    const int pm_bytes = env_int("WLCS_BATCH_PM_KB", 33) * 1024;
+    const int pm_bytes = std::max(env_int("WLCS_BATCH_PM_KB", 33), 14) * 1024;  // >= flags + chunk stage
     const size_t ws_bytes = wlcs::batch_workspace_bytes(uint32_t(pairs), pm_bytes);
     WLCS_CUDA(c.ws.ensure(ws_bytes));
     wlcs::BatchDev d{};
@@ -519,7 +519,7 @@ int batch_host_pipelined(Ctx& c, const uint8_t* xs, const uint64_t* x_off, const
         WLCS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         c.chunk_ev.push_back(e);
     }
-    const int pm_bytes = env_int("WLCS_BATCH_PM_KB", 33) * 1024;
+    const int pm_bytes = std::max(env_int("WLCS_BATCH_PM_KB", 33), 14) * 1024;  // >= flags + chunk stage
     std::vector<size_t> p0(nchunks + 1);
     for (int k = 0; k <= nchunks; ++k) p0[k] = pairs * size_t(k) / size_t(nchunks);
     std::vector<size_t> ws_off(nchunks + 1, 0);
