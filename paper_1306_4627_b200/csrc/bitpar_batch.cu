@@ -465,6 +465,9 @@ __device__ __forceinline__ uint32_t build_task(const BatchDev& d, const LanePair
             const uint32_t woff =
                 lane_off + (wide ? uint32_t((k >> 2) * 512 + (k & 3) * 4) : uint32_t(k * 4));
             sts_u32(pm + woff, 0u);  // code 0: the zero row
+            // codes are dense in byte order and the walk below visits the
+            // present bytes in increasing order: code c's row is one stride on
+            uint32_t caddr = pm + woff;
             // match mask of byte v = h*16 + 4j + i:
             //   hi(h) & b[j] & a[i],  a[i] / b[j] = equality masks of the bit
             //   pairs (planes 0,1) / (planes 2,3), hi(h) = planes 4..7 == h
@@ -478,7 +481,6 @@ __device__ __forceinline__ uint32_t build_task(const BatchDev& d, const LanePair
                     vmask & ~((P[4] ^ (0u - (h & 1u))) | (P[5] ^ (0u - ((h >> 1) & 1u))) |
                               (P[6] ^ (0u - ((h >> 2) & 1u))) | (P[7] ^ (0u - ((h >> 3) & 1u))));
                 const uint32_t nm = lds_u16(inv + 2u * h);
-                const uint32_t mrow = map + h * 16u;
 #pragma unroll
                 for (int jj = 0; jj < 4; ++jj) {
                     if ((nm >> (4 * jj)) & 0xfu) {
@@ -486,8 +488,8 @@ __device__ __forceinline__ uint32_t build_task(const BatchDev& d, const LanePair
 #pragma unroll
                         for (int ii = 0; ii < 4; ++ii) {
                             if ((nm >> (4 * jj + ii)) & 1u) {
-                                const uint32_t c = lds_u8(mrow + uint32_t(4 * jj + ii));
-                                sts_u32(pm + c * cs + woff, hb & a[ii]);
+                                caddr += cs;
+                                sts_u32(caddr, hb & a[ii]);
                             }
                         }
                     }
