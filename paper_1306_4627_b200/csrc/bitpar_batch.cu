@@ -40,6 +40,7 @@ constexpr int kHalfUnroll = WLCS_BATCH_HALF_UNROLL;  // half-chunk loop unroll (
 constexpr int kNumClasses = 6 * kMaxK;   // S in {1,2,4,8,16,32} x K in 1..12
 constexpr int kChunkBuckets = 128;       // chunk-count buckets per class (clamped)
 constexpr int kBuckets = kNumClasses * kChunkBuckets;
+constexpr int kTableSlots = (kNumClasses + 31) / 32;  // task-table entries per lane
 constexpr int kMapBytes = 512;  // map [256] + inverse code list [256]
 constexpr uint32_t kNoBucket = 0xffffffffu;
 
@@ -114,8 +115,10 @@ __global__ void __launch_bounds__(256) batch_plan_kernel(BatchDev d, uint32_t* h
 // ranges and the task table.
 __global__ void __launch_bounds__(1024) batch_scan_kernel(BatchDev d, const uint32_t* hist,
                                                           uint32_t* cursor) {
-    constexpr int kPer = kBuckets / 1024;  // 6
+    constexpr int kPer = kBuckets / 1024;
+    static_assert(kBuckets % 1024 == 0, "scan split");
     __shared__ uint32_t warp_sums[32];
+    __shared__ uint32_t order_start[kNumClasses + 1];
     const int tid = threadIdx.x;
     uint32_t v[kPer];
     uint32_t sum = 0;
@@ -147,24 +150,44 @@ __global__ void __launch_bounds__(1024) batch_scan_kernel(BatchDev d, const uint
     uint32_t run = warp_sums[warp] + incl - sum;
 #pragma unroll
     for (int i = 0; i < kPer; ++i) {
-        cursor[tid * kPer + i] = run;
+        const int b = tid * kPer + i;
+        if (b % kChunkBuckets == 0) order_start[b / kChunkBuckets] = run;
+        cursor[b] = run;
         run += v[i];
     }
+    if (tid == 1023) order_start[kNumClasses] = run;
     __syncthreads();
-    if (tid == 0) {
-        uint32_t ts = 0;
-        for (int o = 0; o < kNumClasses; ++o) {
-            const int c = kNumClasses - 1 - o;
-            const uint32_t per_task = 32u >> (c / kMaxK);
-            const uint32_t start = cursor[o * kChunkBuckets];
-            const uint32_t end = o + 1 < kNumClasses ? cursor[(o + 1) * kChunkBuckets]
-                                                     : cursor[kBuckets - 1] + hist[kBuckets - 1];
-            d.meta[kMetaCount + o] = end - start;
-            d.meta[kMetaPairStart + o] = start;
-            d.meta[kMetaTaskStart + o] = ts;
-            ts += (end - start + per_task - 1) / per_task;
+    if (warp == 0) {
+        // orders 3*lane .. 3*lane+2: counts, starts, task counts, then an
+        // exclusive scan of the task counts in order
+        uint32_t nt[kTableSlots], tsum = 0;
+#pragma unroll
+        for (int q = 0; q < kTableSlots; ++q) {
+            const int o = lane * kTableSlots + q;
+            nt[q] = 0;
+            if (o < kNumClasses) {
+                const uint32_t per_task = 32u >> ((kNumClasses - 1 - o) / kMaxK);
+                const uint32_t cnt = order_start[o + 1] - order_start[o];
+                d.meta[kMetaCount + o] = cnt;
+                d.meta[kMetaPairStart + o] = order_start[o];
+                nt[q] = (cnt + per_task - 1) / per_task;
+            }
+            tsum += nt[q];
         }
-        d.meta[kMetaTaskStart + kNumClasses] = ts;
+        uint32_t ti = tsum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(kFullMask, ti, o);
+            if (lane >= o) ti += t;
+        }
+        uint32_t ts = ti - tsum;
+#pragma unroll
+        for (int q = 0; q < kTableSlots; ++q) {
+            const int o = lane * kTableSlots + q;
+            if (o < kNumClasses) d.meta[kMetaTaskStart + o] = ts;
+            ts += nt[q];
+        }
+        if (lane == 31) d.meta[kMetaTaskStart + kNumClasses] = ti;
     }
 }
 
@@ -214,7 +237,6 @@ struct TaskInfo {
 // constant during the sweep kernel: every lane keeps orders `lane`,
 // `lane + 32` and `lane + 64` in registers, so decoding a task is ballots and
 // shuffles only.
-constexpr int kTableSlots = (kNumClasses + 31) / 32;
 static_assert(kTableSlots == 3, "task table slots");
 struct TaskTable {
     uint32_t ts[kTableSlots], ps[kTableSlots], cn[kTableSlots];
