@@ -766,7 +766,8 @@ int wlcs_length_batch_ex(const uint8_t* xs, const uint64_t* x_off, const uint8_t
     WLCS_CUDA(c->out.ensure(pairs * 4));
     cudaStream_t s = c->stream;
     const int nchunks = variant == WLCS_VARIANT_BITPARALLEL
-                            ? int(std::min<size_t>(8, pairs / 8192))
+                            ? int(std::min<size_t>(size_t(env_int("WLCS_BATCH_CHUNKS", 4)),
+                                                   pairs / 8192))
                             : 1;
     if (nchunks >= 2 && xs_bytes + ys_bytes >= (16u << 20))
         return batch_host_pipelined(*c, xs, x_off, ys, y_off, pairs, nchunks, out);
