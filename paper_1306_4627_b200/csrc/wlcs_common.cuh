@@ -18,6 +18,23 @@ namespace wlcs {
 constexpr unsigned kFullMask = 0xffffffffu;
 constexpr int kRowsPerStep = 16;  // one 16-byte chunk of the row string per step
 
+// Byte-wise gather of a chunk that straddles the allocation end (rare; kept
+// out of line so the callers' hot loops stay small).
+static __device__ __noinline__ uint4 load_chunk16_slow(const uint8_t* p, const uint8_t* alloc_lo,
+                                                const uint8_t* alloc_hi) {
+    uint64_t lo = 0, hi = 0;
+#pragma unroll 1
+    for (int b = 0; b < 16; ++b) {
+        const uint8_t* q = p + b;
+        if (q >= alloc_lo && q < alloc_hi) {
+            const uint64_t v = __ldg(q);
+            if (b < 8) lo |= v << (8 * b);
+            else hi |= v << (8 * (b - 8));
+        }
+    }
+    return make_uint4(uint32_t(lo), uint32_t(lo >> 32), uint32_t(hi), uint32_t(hi >> 32));
+}
+
 // 16 bytes of a string starting at the 16-byte-aligned address `p`.
 // Bytes outside [lo, hi) of the allocation are never touched: when the chunk
 // straddles the allocation end the valid bytes are gathered one by one.
@@ -26,13 +43,7 @@ __device__ __forceinline__ uint4 load_chunk16(const uint8_t* p, const uint8_t* a
     if (p >= alloc_lo && p + 16 <= alloc_hi) {
         return __ldg(reinterpret_cast<const uint4*>(p));
     }
-    uint32_t w[4] = {0, 0, 0, 0};
-#pragma unroll
-    for (int b = 0; b < 16; ++b) {
-        const uint8_t* q = p + b;
-        if (q >= alloc_lo && q < alloc_hi) w[b >> 2] |= uint32_t(__ldg(q)) << (8 * (b & 3));
-    }
-    return make_uint4(w[0], w[1], w[2], w[3]);
+    return load_chunk16_slow(p, alloc_lo, alloc_hi);
 }
 
 // Byte r (0..15) of a 16-byte chunk; r is a compile-time constant in the
