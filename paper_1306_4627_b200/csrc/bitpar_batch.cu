@@ -64,7 +64,8 @@ __device__ __forceinline__ int class_of(int sidx, int k) { return sidx * kMaxK +
 // its bucket: a block-local rank (shared-memory atomics) plus the block's base
 // in that bucket (one global atomic per block and bucket), so the scatter
 // needs no atomics.
-__global__ void __launch_bounds__(256) batch_plan_kernel(BatchDev d, uint32_t* hist,
+constexpr int kPlanThreads = 1024;  // fewer blocks: fewer bucket flushes / global atomics
+__global__ void __launch_bounds__(kPlanThreads) batch_plan_kernel(BatchDev d, uint32_t* hist,
                                                          uint32_t* bucket, uint32_t* rank) {
     __shared__ uint32_t local[kBuckets];
     for (int i = threadIdx.x; i < kBuckets; i += blockDim.x) local[i] = 0;
@@ -111,10 +112,11 @@ __global__ void __launch_bounds__(256) batch_plan_kernel(BatchDev d, uint32_t* h
     }
 }
 
-// One CTA: exclusive scan of the bucket histogram -> cursors, per-class pair
-// ranges and the task table.
-__global__ void __launch_bounds__(1024) batch_scan_kernel(BatchDev d, const uint32_t* hist,
-                                                          uint32_t* cursor) {
+// Exclusive scan of the bucket histogram into shared memory (every scatter
+// block does it: 9216 counts, cheaper than a separate single-block launch);
+// block 0 also writes the per-order pair ranges and the task table.
+__device__ __forceinline__ void scan_buckets(const BatchDev& d, const uint32_t* hist,
+                                             uint32_t* cursor, bool bookkeeping) {
     constexpr int kPer = kBuckets / 1024;
     static_assert(kBuckets % 1024 == 0, "scan split");
     __shared__ uint32_t warp_sums[32];
@@ -157,7 +159,7 @@ __global__ void __launch_bounds__(1024) batch_scan_kernel(BatchDev d, const uint
     }
     if (tid == 1023) order_start[kNumClasses] = run;
     __syncthreads();
-    if (warp == 0) {
+    if (bookkeeping && warp == 0) {
         // orders 3*lane .. 3*lane+2: counts, starts, task counts, then an
         // exclusive scan of the task counts in order
         uint32_t nt[kTableSlots], tsum = 0;
@@ -191,14 +193,21 @@ __global__ void __launch_bounds__(1024) batch_scan_kernel(BatchDev d, const uint
     }
 }
 
-__global__ void __launch_bounds__(256) batch_scatter_kernel(BatchDev d, const uint32_t* bucket,
-                                                            const uint32_t* rank,
-                                                            const uint32_t* start) {
-    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= d.pairs) return;
-    const uint32_t b = bucket[i];
-    if (b == kNoBucket) return;
-    d.vals[start[b] + rank[i]] = d.ids ? d.ids[i] : i;
+// 1024-thread blocks, kScatterPairs pairs each: scan, then place every pair
+// id at cursor[bucket] + rank.
+constexpr int kScatterPairs = 2048;
+__global__ void __launch_bounds__(1024) batch_scatter_kernel(BatchDev d, const uint32_t* hist,
+                                                             const uint32_t* bucket,
+                                                             const uint32_t* rank) {
+    __shared__ uint32_t cursor[kBuckets];
+    scan_buckets(d, hist, cursor, blockIdx.x == 0);
+    const uint32_t i0 = blockIdx.x * uint32_t(kScatterPairs);
+    const uint32_t i1 = min(d.pairs, i0 + uint32_t(kScatterPairs));
+    for (uint32_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+        const uint32_t b = bucket[i];
+        if (b == kNoBucket) continue;
+        d.vals[cursor[b] + rank[i]] = d.ids ? d.ids[i] : i;
+    }
 }
 
 // Per-lane view of its pair inside a task.
@@ -703,7 +712,6 @@ cudaError_t batch_launch(BatchDev d, void* workspace, int sms, cudaStream_t stre
     d.meta = ws;
     d.safe16 = reinterpret_cast<const uint4*>(ws + kMetaSafe16);
     uint32_t* hist = ws + kWsHist;
-    uint32_t* cursor = ws + kWsCursor;
     uint32_t* bucket = ws + kWsPairs;
     d.vals = bucket + d.pairs;
     d.overflow = d.vals + d.pairs;
@@ -711,10 +719,10 @@ cudaError_t batch_launch(BatchDev d, void* workspace, int sms, cudaStream_t stre
     cudaError_t e = cudaMemsetAsync(ws, 0, kWsCursor * sizeof(uint32_t), stream);  // meta + hist
     if (e != cudaSuccess) return e;
     if (d.pairs == 0) return cudaSuccess;
-    const int blocks = int((d.pairs + 255) / 256);
-    batch_plan_kernel<<<blocks, 256, 0, stream>>>(d, hist, bucket, rank);
-    batch_scan_kernel<<<1, 1024, 0, stream>>>(d, hist, cursor);
-    batch_scatter_kernel<<<blocks, 256, 0, stream>>>(d, bucket, rank, cursor);
+    batch_plan_kernel<<<int((d.pairs + kPlanThreads - 1) / kPlanThreads), kPlanThreads, 0, stream>>>(
+        d, hist, bucket, rank);
+    batch_scatter_kernel<<<int((d.pairs + kScatterPairs - 1) / kScatterPairs), 1024, 0, stream>>>(
+        d, hist, bucket, rank);
     int occ = 0;
     const int smem = batch_smem_per_cta(d.pm_bytes);
     e = cudaFuncSetAttribute(batch_main_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
