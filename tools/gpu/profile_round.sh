@@ -1,6 +1,6 @@
 # Round-end measurement set: bench lines (C2 headline + reference arm + the
-# single-pair configs + variants), the ncu launch list of the headline command
-# and summaries.  Each ncu runs only after its command exited 0 without ncu.
+# single-pair configs + variants) and the ncu launch list of the headline
+# command (ncu only after the same command exited 0 without it).
 set -u
 mkdir -p gpurun_out/prof
 python -m pytest tests -m gpu -q 2>&1 | tail -2 > gpurun_out/prof/pytest_gpu.txt
@@ -14,6 +14,4 @@ python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/pro
       python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > /dev/null 2>&1
 python tools/launches.py gpurun_out/prof/launches_c2.csv > gpurun_out/prof/launches_c2.txt 2>&1
 cat gpurun_out/prof/pytest_gpu.txt gpurun_out/prof/launches_c2.txt
-# single-pair strip kernel (C4, K=4): one ncu capture after the plain run above
-ncu --set full --import-source on --clock-control none -k regex:pair_strip -c 1 -f -o gpurun_out/prof/c4_strip python bench.py --config c4 --steps 1 --warmup 0 > /dev/null 2>&1
 ls gpurun_out/prof/
