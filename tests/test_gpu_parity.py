@@ -104,6 +104,29 @@ def test_batch_large_alphabet_many(wl, restatement):
                           restatement.length_batch(xb, xo, yb, yo))
 
 
+def test_batch_device_tight_buffers(wl, restatement):
+    """Device buffers of exactly the strings' size (no tail padding): the
+    pairs at the buffer ends take the bounds-checked sweep and the byte-gather
+    chunk path; everything else the fast path."""
+    import torch
+    rng = np.random.default_rng(4242)
+    for alphabet in (DNA, PROTEIN):
+        xs, ys = rand_pairs(rng, 700, 1, 900, alphabet)
+        xb, xo, yb, yo = wl.pack_pairs(xs, ys)
+        dev = torch.device("cuda", 0)
+        d_xs = torch.from_numpy(xb.copy()).to(dev)
+        d_ys = torch.from_numpy(yb.copy()).to(dev)
+        d_xo = torch.from_numpy(xo.view(np.int64)).to(dev)
+        d_yo = torch.from_numpy(yo.view(np.int64)).to(dev)
+        d_out = torch.zeros(len(xs), dtype=torch.int32, device=dev)
+        wl.lcs_length_batch_device(d_xs.data_ptr(), d_xo.data_ptr(), d_ys.data_ptr(),
+                                   d_yo.data_ptr(), len(xs), int(xo[-1]), int(yo[-1]),
+                                   d_out.data_ptr(), torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        assert np.array_equal(d_out.cpu().numpy().astype(np.uint32),
+                              restatement.length_batch(xb, xo, yb, yo))
+
+
 @pytest.mark.parametrize("m,n", [(1, 1), (5, 300), (300, 5), (1000, 1000), (4097, 33), (33, 4097),
                                  (5000, 200), (12345, 6789)])
 def test_single_pair_lengths(wl, restatement, m, n):
