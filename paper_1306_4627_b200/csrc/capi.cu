@@ -164,9 +164,10 @@ struct PairPlan {
 
 // Words per lane.  Cost model in cycles, calibrated on B200 (single-strip
 // probe, tools/pair_probe.py): a 16-row step costs kStep[K] cycles when the
-// strip has a sub-partition to itself; strips start ~60 steps apart (lane
-// pipeline + hand-off); strips beyond the resident warps run in waves; more
-// resident strips than sub-partitions share issue slots.
+// strip has a sub-partition to itself; strips start ~40 steps apart (31-step
+// lane pipeline + carry hand-off; tools/gpu/skew.sh); strips beyond the
+// resident warps run in waves; more resident strips than sub-partitions share
+// issue slots.
 int batch_kmax() {
     const int k = env_int("WLCS_BATCH_KMAX", 12);
     return k >= 1 && k <= 12 ? k : 12;
@@ -188,7 +189,7 @@ int choose_k(const Ctx& c, int64_t W, int64_t rows_per_prob, int sigma, int npro
         const double active = std::min(total, per_sm * c.sms);
         const double share = std::max(1.0, active / (4.0 * c.sms));
         const double waves = std::ceil(total / active);
-        const double cost = (waves * chunks + strips * 60.0) * step * share;
+        const double cost = (waves * chunks + strips * 40.0) * step * share;
         if (cost < best) {
             best = cost;
             best_k = K;
