@@ -29,6 +29,7 @@
 //   otherwise                  -> Left
 // so per row it only needs the highest set bit of (PM[x_i] | ~V_i) at or
 // below column j: one row per iteration instead of one cell.
+#include <cstdio>
 #include <cstdlib>
 
 #include "sweep.cuh"
@@ -454,7 +455,111 @@ __device__ __forceinline__ int64_t walk_cand(int64_t guess, int l, int64_t N) {
     return c < 0 ? 0 : (c > N ? N : c);
 }
 
-// 1. one CTA (kWalkCand threads) per block of rows
+// Warp-cooperative walk of DP rows top, top-1, ..., lo+1 entering row `top`
+// at column j.  The serial walk costs one dependent global round trip per
+// row; here the warp loads, for the next 32 rows at once (lane l: row top-l),
+// the three mask words wt, wt-1, wt-2 under the entry column (E = PM | ~V and
+// PM), then steps through the rows in registers, row l's words fetched by
+// shuffles (they do not depend on j, so they are issued ahead).  The path
+// only moves left, so the 96-column window lasts until it is left (then it is
+// reloaded at the current row).  visit(i, j_exit, diag) runs (warp-uniform)
+// for every row walked and returns false to stop; once j reaches 0 the
+// remaining rows exit at 0 without emitting and are not visited.  Returns the
+// block's exit column.
+template <int K, typename Visit>
+__device__ __forceinline__ int64_t warp_walk(const FillProblem& P, int64_t top, int64_t lo,
+                                             int64_t j, Visit visit) {
+    const int lane = int(lane_id());
+    int64_t i = top;
+    bool stop = false;
+    // loop and branch conditions go through warp votes: they are warp-uniform
+    // by construction, and the votes let the compiler see that (otherwise the
+    // shuffles below get the slow collective emulation)
+    while (__all_sync(kFullMask, i > lo && j > 0 && !stop)) {
+        const int64_t wt = (j - 1) >> 5;
+        const int64_t q = i - 1 - lane;  // 0-based row of this lane
+        uint32_t E0 = 0, E1 = 0, E2 = 0, Q0 = 0, Q1 = 0, Q2 = 0;
+        if (q >= lo) {
+            const uint32_t* pmrow = P.pmg + int64_t(walk_code<K>(P, q)) * P.W;
+            Q0 = __ldg(pmrow + wt);
+            E0 = Q0 | ~P.rows_out[pair_row_index(q, wt, K, P.Dpad)];
+            if (wt >= 1) {
+                Q1 = __ldg(pmrow + wt - 1);
+                E1 = Q1 | ~P.rows_out[pair_row_index(q, wt - 1, K, P.Dpad)];
+            }
+            if (wt >= 2) {
+                Q2 = __ldg(pmrow + wt - 2);
+                E2 = Q2 | ~P.rows_out[pair_row_index(q, wt - 2, K, P.Dpad)];
+            }
+        }
+        const int nrows = int(i - lo < 32 ? i - lo : 32);
+        int done = 0;
+        bool go = true;
+#pragma unroll 8
+        for (int l = 0; l < 32; ++l) {
+            const uint32_t e0 = __shfl_sync(kFullMask, E0, l), e1 = __shfl_sync(kFullMask, E1, l),
+                           e2 = __shfl_sync(kFullMask, E2, l);
+            const uint32_t q0 = __shfl_sync(kFullMask, Q0, l), q1 = __shfl_sync(kFullMask, Q1, l),
+                           q2 = __shfl_sync(kFullMask, Q2, l);
+            if (__all_sync(kFullMask, go && l < nrows)) {
+                const int64_t jm = j - 1;
+                const int d = int(wt - (jm >> 5));  // window word holding column j-1
+                const uint32_t top_mask = (2u << (jm & 31)) - 1u;
+                // masked words from the entry word down to the window bottom
+                const uint32_t a = d == 0 ? (e0 & top_mask) : d == 1 ? (e1 & top_mask) : (e2 & top_mask);
+                const uint32_t b = d == 0 ? e1 : d == 1 ? e2 : 0u;
+                const uint32_t c = d == 0 ? e2 : 0u;
+                const uint32_t qa = d == 0 ? q0 : d == 1 ? q1 : q2;
+                const uint32_t qb = d == 0 ? q1 : d == 1 ? q2 : 0u;
+                const uint32_t qc = d == 0 ? q2 : 0u;
+                const int64_t wa = wt - d;  // word index of a
+                int64_t h = -1;
+                uint32_t dg = 0;
+                if (d > 2) {
+                    go = false;  // entry column left the window: reload here
+                } else if (a) {
+                    const int bb = 31 - __clz(a);
+                    h = wa * 32 + bb;
+                    dg = (qa >> bb) & 1u;
+                } else if (b) {
+                    const int bb = 31 - __clz(b);
+                    h = (wa - 1) * 32 + bb;
+                    dg = (qb >> bb) & 1u;
+                } else if (c) {
+                    const int bb = 31 - __clz(c);
+                    h = (wa - 2) * 32 + bb;
+                    dg = (qc >> bb) & 1u;
+                } else if (wt - 2 > 0) {
+                    go = false;  // no set bit inside the window, more words below
+                }
+                if (go) {
+                    j = h < 0 ? 0 : h + 1 - int64_t(dg);  // no set bit at all: Left to 0
+                    done = l + 1;
+                    if (!visit(i - l, j, dg)) {
+                        stop = true;
+                        go = false;
+                    } else if (j == 0) {
+                        go = false;
+                    }
+                }
+            }
+        }
+        i -= done;
+        if (__all_sync(kFullMask, done == 0 && !stop && i > lo && j > 0)) {
+            // the next set bit lies more than the window below the entry:
+            // one serial row step (warp-uniform), then a fresh window
+            uint32_t dg;
+            j = walk_step<K>(P, walk_code<K>(P, i - 1), i - 1, j, &dg);
+            if (!visit(i, j, dg)) stop = true;
+            --i;
+        }
+    }
+    return j;
+}
+
+// 1. one CTA (kWalkCand threads) per block of rows, one thread per candidate
+// (thousands of independent walks: the row latency is hidden by parallelism)
+constexpr int kWalkWarps = 4;  // warps per CTA of the warp-walk kernels
 template <int K>
 __global__ void __launch_bounds__(kWalkCand) walk_spec_kernel(PairDev d, int32_t* exits,
                                                               int32_t* ckpt) {
@@ -478,83 +583,113 @@ __global__ void __launch_bounds__(kWalkCand) walk_spec_kernel(PairDev d, int32_t
     exits[k * kWalkCand + threadIdx.x] = int32_t(j);
 }
 
-// 2. one thread; entry[k] = true entry column of block k
+// 2. one warp (sequential over blocks, bottom first); entry[k] = true entry
+// column of block k
 template <int K>
-__global__ void walk_resolve_kernel(PairDev d, const int32_t* exits, const int32_t* ckpt,
-                                    int32_t* entry, uint32_t* misses) {
+__global__ void __launch_bounds__(32) walk_resolve_kernel(PairDev d, const int32_t* exits,
+                                                          const int32_t* ckpt, int32_t* entry,
+                                                          uint32_t* misses) {
     const FillProblem& P = d.prob[0];
     const int64_t M = P.rows, N = P.cols;
     const int64_t nb = (M + kWalkRows - 1) / kWalkRows;
+    const int lane = int(lane_id());
     int64_t j = N;
     uint32_t miss = 0;
+    // candidate exits are staged into shared memory 32 blocks at a time
+    // (cp.async, the next group in flight while the current one is used): the
+    // bottom-up chain over the blocks reads shared memory, not global
+    constexpr int kGroup = 32;
+    __shared__ __align__(16) int32_t exs[2][kGroup * kWalkCand];
+    auto stage = [&](int64_t grp) {
+        const int64_t k0 = grp * kGroup;
+        if (k0 < nb) {
+            const int64_t n16 = ((nb - k0 < kGroup ? nb - k0 : kGroup) * kWalkCand) / 4;
+            const int4* src = reinterpret_cast<const int4*>(exits + k0 * kWalkCand);
+            const uint32_t dst = uint32_t(__cvta_generic_to_shared(&exs[grp & 1][0]));
+            for (int64_t t = lane; t < n16; t += 32)
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + uint32_t(t) * 16u),
+                             "l"(src + t)
+                             : "memory");
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    stage(0);
+    stage(1);
     for (int64_t k = 0; k < nb; ++k) {
-        entry[k] = int32_t(j);
+        if (lane == 0) entry[k] = int32_t(j);
+        if (k % kGroup == 0) {
+            asm volatile("cp.async.wait_group 1;" ::: "memory");  // group k / kGroup landed
+            __syncwarp();
+        }
+        const int32_t* exl = &exs[(k / kGroup) & 1][(k % kGroup) * kWalkCand];
         const int64_t top = M - k * kWalkRows;
         const int64_t lo = top - kWalkRows > 0 ? top - kWalkRows : 0;
         const int64_t g = walk_guess(top, M, N);
         const int32_t* ex = exits + k * kWalkCand;
+        auto ex_at = [&](int64_t l) { return int64_t(exl[l]); };
         int64_t next = -1;
         // bracketing candidates (candidate columns are non-decreasing in l)
         const int64_t l0 = (j - walk_cand(g, 0, N)) / kWalkStride;
         for (int64_t l = l0 - 1; l <= l0 + 1 && next < 0; ++l) {
             if (l < 0 || l >= kWalkCand) continue;
+            const int64_t el = ex_at(l);
+            const int64_t el1 = ex_at(l + 1 < kWalkCand ? l + 1 : l);
             const int64_t ca = walk_cand(g, int(l), N);
-            if (ca == j) next = ex[l];
-            else if (l + 1 < kWalkCand && ca < j && j < walk_cand(g, int(l + 1), N) &&
-                     ex[l] == ex[l + 1])
-                next = ex[l];
+            if (ca == j) next = el;
+            else if (l + 1 < kWalkCand && ca < j && j < walk_cand(g, int(l + 1), N) && el == el1)
+                next = el;
         }
-        if (next < 0) {
+        if (__all_sync(kFullMask, next < 0)) {
             // Outside the window or the bracket had not merged at the block's
             // end: walk from the true entry, but stop at the first checkpoint
             // where the walk meets a candidate's recorded column (from there
             // on it IS that candidate's path).
             ++miss;
             const int32_t* ck = ckpt + k * (kWalkNCkpt * kWalkCand);
-            int64_t lb = l0 < 0 ? 0 : (l0 >= kWalkCand ? kWalkCand - 1 : l0);
-            int64_t jw = j;
-            for (int64_t i = top; i > lo; --i) {
-                uint32_t dg;
-                if (jw > 0) jw = walk_step<K>(P, walk_code<K>(P, i - 1), i - 1, jw, &dg);
-                const int64_t done = top - i + 1;
-                if (done % kWalkCkpt == 0 && done < kWalkRows) {
-                    const int32_t* row = ck + (done / kWalkCkpt) * kWalkCand;
-                    int64_t hit = -1;
+            const int64_t lb = l0 < 0 ? 0 : (l0 >= kWalkCand ? kWalkCand - 1 : l0);
+            int64_t hit = -1;
+            const int64_t jw = warp_walk<K>(P, top, lo, j, [&](int64_t i, int64_t jx, uint32_t) {
+                const int64_t walked = top - i + 1;
+                if (walked % kWalkCkpt == 0 && walked < kWalkRows) {
+                    const int32_t* row = ck + (walked / kWalkCkpt) * kWalkCand;
                     for (int64_t l = lb - 1; l <= lb + 1 && hit < 0; ++l)
-                        if (l >= 0 && l < kWalkCand && row[l] == jw) hit = l;
-                    if (hit >= 0) {
-                        next = ex[hit];
-                        break;
-                    }
+                        if (l >= 0 && l < kWalkCand && row[l] == jx) hit = l;
+                    if (hit >= 0) return false;
                 }
-            }
-            if (next < 0) next = jw;
+                return true;
+            });
+            next = hit >= 0 ? ex[hit] : jw;
         }
         j = next;
+        if (k % kGroup == kGroup - 1) {
+            __syncwarp();  // everyone done with this buffer before it is refilled
+            stage(k / kGroup + 2);
+        }
     }
-    *misses = miss;
+    if (lane == 0) *misses = miss;
 }
 
-// 3. one thread per block: flags[q] = 1 iff row q emits; counts[k]
+// 3. one warp per block: flags[q] = 1 iff row q emits (flags pre-zeroed);
+// counts[k]
 template <int K>
-__global__ void walk_emit_kernel(PairDev d, const int32_t* entry, uint8_t* flags,
-                                 uint32_t* counts) {
+__global__ void __launch_bounds__(32 * kWalkWarps) walk_emit_kernel(PairDev d, const int32_t* entry,
+                                                                    uint8_t* flags,
+                                                                    uint32_t* counts) {
     const FillProblem& P = d.prob[0];
     const int64_t M = P.rows;
     const int64_t nb = (M + kWalkRows - 1) / kWalkRows;
-    const int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (k >= nb) return;
+    const int64_t k = int64_t(blockIdx.x) * kWalkWarps + (threadIdx.x >> 5);
+    if (__all_sync(kFullMask, k >= nb)) return;
+    const int lane = int(lane_id());
     const int64_t top = M - k * kWalkRows;
     const int64_t lo = top - kWalkRows > 0 ? top - kWalkRows : 0;
-    int64_t j = entry[k];
     uint32_t n = 0;
-    for (int64_t i = top; i > lo; --i) {
-        uint32_t dg = 0;
-        if (j > 0) j = walk_step<K>(P, walk_code<K>(P, i - 1), i - 1, j, &dg);
-        flags[i - 1] = uint8_t(dg);
+    warp_walk<K>(P, top, lo, entry[k], [&](int64_t i, int64_t, uint32_t dg) {
         n += dg;
-    }
-    counts[k] = n;
+        if (lane == 0 && dg) flags[i - 1] = 1;
+        return true;
+    });
+    if (lane == 0) counts[k] = n;
 }
 
 // 4a. one thread: output offsets (forward order = blocks from the top rows)
@@ -830,12 +965,31 @@ cudaError_t pair_walk(const PairDev& d, int K, const uint8_t* x, uint8_t* out,
     uint8_t* flags = reinterpret_cast<uint8_t*>(offsets + nb);
     const int tb = 128;
     const int eb = int((nb + tb - 1) / tb);
+    const int emit_ctas = int((nb + kWalkWarps - 1) / kWalkWarps);
+    cudaError_t e = cudaMemsetAsync(flags, 0, size_t(M), stream);
+    if (e != cudaSuccess) return e;
+    const bool dbg = getenv("WLCS_DEBUG_WALK") != nullptr;
+    cudaEvent_t ev[6];
+    if (dbg) for (auto& x : ev) cudaEventCreate(&x);
+    auto mark = [&](int i) { if (dbg) cudaEventRecord(ev[i], stream); };
     auto run = [&](auto spec, auto resolve, auto emit) {
+        mark(0);
         spec<<<int(nb), kWalkCand, 0, stream>>>(d, exits, ckpt);
-        resolve<<<1, 1, 0, stream>>>(d, exits, ckpt, entry, misses);
-        emit<<<eb, tb, 0, stream>>>(d, entry, flags, counts);
+        mark(1);
+        resolve<<<1, 32, 0, stream>>>(d, exits, ckpt, entry, misses);
+        mark(2);
+        emit<<<emit_ctas, 32 * kWalkWarps, 0, stream>>>(d, entry, flags, counts);
+        mark(3);
         walk_scan_kernel<<<1, 1, 0, stream>>>(counts, nb, offsets, out_len);
         walk_write_kernel<<<eb, tb, 0, stream>>>(x, M, flags, offsets, out);
+        mark(4);
+        if (dbg) {
+            cudaEventSynchronize(ev[4]);
+            float t[4];
+            for (int i = 0; i < 4; ++i) cudaEventElapsedTime(&t[i], ev[i], ev[i + 1]);
+            fprintf(stderr, "wlcs walk ms: spec %.3f resolve %.3f emit %.3f scan+write %.3f\n", t[0],
+                    t[1], t[2], t[3]);
+        }
         return cudaGetLastError();
     };
     switch (K) {
