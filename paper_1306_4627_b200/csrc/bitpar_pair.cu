@@ -502,18 +502,19 @@ __device__ __forceinline__ int64_t warp_walk(const FillProblem& P, int64_t top, 
             const uint32_t q0 = __shfl_sync(kFullMask, Q0, l), q1 = __shfl_sync(kFullMask, Q1, l),
                            q2 = __shfl_sync(kFullMask, Q2, l);
             if (__all_sync(kFullMask, go && l < nrows)) {
-                const int64_t jm = j - 1;
-                const int d = int(wt - (jm >> 5));  // window word holding column j-1
+                // 32-bit column arithmetic (columns < 2^31)
+                const int jm = int(j) - 1;
+                const int d = int(wt) - (jm >> 5);  // window word holding column j-1
                 const uint32_t top_mask = (2u << (jm & 31)) - 1u;
                 // masked words from the entry word down to the window bottom
-                const uint32_t a = d == 0 ? (e0 & top_mask) : d == 1 ? (e1 & top_mask) : (e2 & top_mask);
+                const uint32_t a = (d == 0 ? e0 : d == 1 ? e1 : e2) & top_mask;
                 const uint32_t b = d == 0 ? e1 : d == 1 ? e2 : 0u;
                 const uint32_t c = d == 0 ? e2 : 0u;
                 const uint32_t qa = d == 0 ? q0 : d == 1 ? q1 : q2;
                 const uint32_t qb = d == 0 ? q1 : d == 1 ? q2 : 0u;
                 const uint32_t qc = d == 0 ? q2 : 0u;
-                const int64_t wa = wt - d;  // word index of a
-                int64_t h = -1;
+                const int wa = int(wt) - d;  // word index of a
+                int h = -1;
                 uint32_t dg = 0;
                 if (d > 2) {
                     go = false;  // entry column left the window: reload here
@@ -533,7 +534,7 @@ __device__ __forceinline__ int64_t warp_walk(const FillProblem& P, int64_t top, 
                     go = false;  // no set bit inside the window, more words below
                 }
                 if (go) {
-                    j = h < 0 ? 0 : h + 1 - int64_t(dg);  // no set bit at all: Left to 0
+                    j = h < 0 ? 0 : int64_t(h + 1 - int(dg));  // no set bit at all: Left to 0
                     done = l + 1;
                     if (!visit(i - l, j, dg)) {
                         stop = true;
@@ -595,6 +596,8 @@ __global__ void __launch_bounds__(32) walk_resolve_kernel(PairDev d, const int32
     const int lane = int(lane_id());
     int64_t j = N;
     uint32_t miss = 0;
+    const long long t_start = clock64();
+    long long t_miss = 0;
     // candidate exits are staged into shared memory 32 blocks at a time
     // (cp.async, the next group in flight while the current one is used): the
     // bottom-up chain over the blocks reads shared memory, not global
@@ -645,20 +648,29 @@ __global__ void __launch_bounds__(32) walk_resolve_kernel(PairDev d, const int32
             // where the walk meets a candidate's recorded column (from there
             // on it IS that candidate's path).
             ++miss;
+            const long long t0 = clock64();
             const int32_t* ck = ckpt + k * (kWalkNCkpt * kWalkCand);
-            const int64_t lb = l0 < 0 ? 0 : (l0 >= kWalkCand ? kWalkCand - 1 : l0);
+            // every checkpoint row is compared against all candidates at once
+            // (4 per lane, one ballot): the walk has drifted since its entry
             int64_t hit = -1;
             const int64_t jw = warp_walk<K>(P, top, lo, j, [&](int64_t i, int64_t jx, uint32_t) {
                 const int64_t walked = top - i + 1;
                 if (walked % kWalkCkpt == 0 && walked < kWalkRows) {
-                    const int32_t* row = ck + (walked / kWalkCkpt) * kWalkCand;
-                    for (int64_t l = lb - 1; l <= lb + 1 && hit < 0; ++l)
-                        if (l >= 0 && l < kWalkCand && row[l] == jx) hit = l;
-                    if (hit >= 0) return false;
+                    const int4 r4 = reinterpret_cast<const int4*>(
+                        ck + (walked / kWalkCkpt) * kWalkCand)[lane];
+                    const int32_t jv = int32_t(jx);
+                    const int sub = r4.x == jv ? 0 : r4.y == jv ? 1 : r4.z == jv ? 2 : r4.w == jv ? 3 : -1;
+                    const uint32_t hits = __ballot_sync(kFullMask, sub >= 0);
+                    if (hits) {
+                        const int src = __ffs(hits) - 1;
+                        hit = int64_t(src) * 4 + __shfl_sync(kFullMask, sub, src);
+                        return false;
+                    }
                 }
                 return true;
             });
             next = hit >= 0 ? ex[hit] : jw;
+            t_miss += clock64() - t0;
         }
         j = next;
         if (k % kGroup == kGroup - 1) {
@@ -666,7 +678,11 @@ __global__ void __launch_bounds__(32) walk_resolve_kernel(PairDev d, const int32
             stage(k / kGroup + 2);
         }
     }
-    if (lane == 0) *misses = miss;
+    if (lane == 0) {
+        misses[0] = miss;
+        misses[1] = uint32_t(t_miss >> 10);                    // diagnostics: kilocycles in
+        misses[2] = uint32_t((clock64() - t_start) >> 10);     // fallback walks / in total
+    }
 }
 
 // 3. one warp per block: flags[q] = 1 iff row q emits (flags pre-zeroed);

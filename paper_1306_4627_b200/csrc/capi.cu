@@ -718,10 +718,12 @@ int wlcs_subsequence(const uint8_t* x, size_t m, const uint8_t* y, size_t n,
     WLCS_CUDA(cudaStreamSynchronize(c->stream));
     if (c->timing) WLCS_CUDA(cudaEventElapsedTime(&c->last_main_ms, c->ev0, c->ev1));
     if (env_int("WLCS_DEBUG_WALK", 0)) {
-        uint32_t miss = 0;
-        WLCS_CUDA(cudaMemcpy(&miss, dmiss, 4, cudaMemcpyDeviceToHost));
-        std::fprintf(stderr, "wlcs walk: %u of %lld blocks resolved by a fallback walk\n", miss,
-                     (long long)((m + 255) / 256));
+        uint32_t miss[3] = {0, 0, 0};
+        WLCS_CUDA(cudaMemcpy(miss, dmiss, 12, cudaMemcpyDeviceToHost));
+        std::fprintf(stderr,
+                     "wlcs walk: %u of %lld blocks resolved by a fallback walk (resolve: %u of "
+                     "%u kcycles in fallbacks)\n",
+                     miss[0], (long long)((m + 255) / 256), miss[1], miss[2]);
     }
     if (len != zeros)
         return fail(WLCS_E_INTERNAL, "traceback length " + std::to_string(len) +

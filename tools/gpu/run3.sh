@@ -1,5 +1,3 @@
-python -m pytest tests -m gpu -q -x 2>&1 | tail -1
-for g in 1 0; do WLCS_PAIR_GEN=$g WLCS_DEBUG_PAIR=1 timeout 300 python bench.py --config c5 --steps 3 --warmup 1 > gpurun_out/k.json 2>gpurun_out/k.err; grep "wlcs pair" gpurun_out/k.err | head -1; python3 -c "
-import json;d=json.load(open('gpurun_out/k.json'));print('gen=$g c5', d['ms_per_step'], d.get('fill_kernel_ms'), d['config'].get('lcs_length'))" 2>&1 | tail -1; done
-for K in 1 2 4; do WLCS_PAIR_K=$K WLCS_DEBUG_PAIR=1 timeout 300 python bench.py --config c5 --steps 3 --warmup 1 > gpurun_out/k.json 2>gpurun_out/k.err; grep "wlcs pair" gpurun_out/k.err | head -1; python3 -c "
-import json;d=json.load(open('gpurun_out/k.json'));print('K=$K c5', d['ms_per_step'], d.get('fill_kernel_ms'))" 2>&1 | tail -1; done
+python -m pytest tests/test_gpu_parity.py -q -x -k "subsequence or golden or c1 or c3 or checkpoint" 2>&1 | tail -2
+for c in c1 c3; do WLCS_DEBUG_WALK=1 timeout 300 python bench.py --config $c --steps 5 --warmup 2 > gpurun_out/b.json 2>gpurun_out/b.err; grep "wlcs walk" gpurun_out/b.err | head -1; python3 -c "
+import json,sys;d=json.load(open('gpurun_out/b.json'));print('$c',d['ms_per_step'],d.get('fill_kernel_ms'),d['config'].get('lcs_length'))" 2>&1 | tail -1; done
