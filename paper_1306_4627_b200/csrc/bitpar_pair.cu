@@ -603,8 +603,10 @@ __global__ void __launch_bounds__(32) walk_resolve_kernel(PairDev d, const int32
     // bottom-up chain over the blocks reads shared memory, not global
     constexpr int kGroup = 32;
     __shared__ __align__(16) int32_t exs[2][kGroup * kWalkCand];
+    __shared__ int64_t gs[2][kGroup];  // the blocks' diagonal guesses
     auto stage = [&](int64_t grp) {
         const int64_t k0 = grp * kGroup;
+        if (k0 + lane < nb) gs[grp & 1][lane] = walk_guess(M - (k0 + lane) * kWalkRows, M, N);
         if (k0 < nb) {
             const int64_t n16 = ((nb - k0 < kGroup ? nb - k0 : kGroup) * kWalkCand) / 4;
             const int4* src = reinterpret_cast<const int4*>(exits + k0 * kWalkCand);
@@ -627,20 +629,35 @@ __global__ void __launch_bounds__(32) walk_resolve_kernel(PairDev d, const int32
         const int32_t* exl = &exs[(k / kGroup) & 1][(k % kGroup) * kWalkCand];
         const int64_t top = M - k * kWalkRows;
         const int64_t lo = top - kWalkRows > 0 ? top - kWalkRows : 0;
-        const int64_t g = walk_guess(top, M, N);
+        const int64_t g = gs[(k / kGroup) & 1][k % kGroup];
         const int32_t* ex = exits + k * kWalkCand;
-        auto ex_at = [&](int64_t l) { return int64_t(exl[l]); };
         int64_t next = -1;
-        // bracketing candidates (candidate columns are non-decreasing in l)
-        const int64_t l0 = (j - walk_cand(g, 0, N)) / kWalkStride;
-        for (int64_t l = l0 - 1; l <= l0 + 1 && next < 0; ++l) {
-            if (l < 0 || l >= kWalkCand) continue;
-            const int64_t el = ex_at(l);
-            const int64_t el1 = ex_at(l + 1 < kWalkCand ? l + 1 : l);
-            const int64_t ca = walk_cand(g, int(l), N);
-            if (ca == j) next = el;
-            else if (l + 1 < kWalkCand && ca < j && j < walk_cand(g, int(l + 1), N) && el == el1)
-                next = el;
+        // bracketing candidates (candidate columns are non-decreasing in l),
+        // l in [l0 - 1, l0 + 1]: lane t tests candidates 4t .. 4t+3 at once;
+        // any candidate that qualifies gives the true exit
+        {
+            const int64_t l0 = (j - walk_cand(g, 0, N)) / kWalkStride;
+            const int4 e4 = *reinterpret_cast<const int4*>(exl + 4 * lane);
+            const int32_t e5 = lane < 31 ? exl[4 * lane + 4] : e4.w;
+            const int32_t ev[5] = {e4.x, e4.y, e4.z, e4.w, e5};
+            int found = -1;
+#pragma unroll
+            for (int sub = 0; sub < 4; ++sub) {
+                const int64_t l = 4 * lane + sub;
+                if (found < 0 && l >= l0 - 1 && l <= l0 + 1) {
+                    const int64_t ca = walk_cand(g, int(l), N);
+                    if (ca == j ||
+                        (l + 1 < kWalkCand && ca < j && j < walk_cand(g, int(l + 1), N) &&
+                         ev[sub] == ev[sub + 1]))
+                        found = sub;
+                }
+            }
+            const uint32_t any = __ballot_sync(kFullMask, found >= 0);
+            if (any) {
+                const int src = __ffs(any) - 1;
+                const int fs = __shfl_sync(kFullMask, found, src);
+                next = exl[4 * src + fs];
+            }
         }
         if (__all_sync(kFullMask, next < 0)) {
             // Outside the window or the bracket had not merged at the block's
@@ -719,17 +736,36 @@ __global__ void walk_scan_kernel(const uint32_t* counts, int64_t nb, uint32_t* o
     *total = run;
 }
 
-// 4b. one thread per block writes its emitted bytes in row order
-__global__ void walk_write_kernel(const uint8_t* x, int64_t M, const uint8_t* flags,
-                                  const uint32_t* offsets, uint8_t* out) {
+// 4b. one warp per block writes its emitted bytes in row order: lane t
+// takes 8 consecutive rows, a warp scan gives its output position
+__global__ void __launch_bounds__(128) walk_write_kernel(const uint8_t* x, int64_t M,
+                                                         const uint8_t* flags,
+                                                         const uint32_t* offsets, uint8_t* out) {
+    static_assert(kWalkRows == 256, "8 rows per lane");
     const int64_t nb = (M + kWalkRows - 1) / kWalkRows;
-    const int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (k >= nb) return;
+    const int64_t k = int64_t(blockIdx.x) * 4 + (threadIdx.x >> 5);
+    if (__all_sync(kFullMask, k >= nb)) return;
+    const int lane = int(lane_id());
     const int64_t top = M - k * kWalkRows;
     const int64_t lo = top - kWalkRows > 0 ? top - kWalkRows : 0;
-    uint8_t* o = out + offsets[k];
-    for (int64_t q = lo; q < top; ++q)
-        if (flags[q]) *o++ = x[q];
+    const int64_t q0 = lo + 8 * lane;
+    uint32_t f = 0, n = 0;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+        const bool e = q0 + r < top && flags[q0 + r];
+        f |= uint32_t(e) << r;
+        n += e;
+    }
+    uint32_t incl = n;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(kFullMask, incl, o);
+        if (lane >= o) incl += t;
+    }
+    uint8_t* o = out + offsets[k] + (incl - n);
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+        if ((f >> r) & 1u) *o++ = x[q0 + r];
 }
 
 // ---- the reference's full tables from the stored bit rows ----------------
@@ -979,8 +1015,6 @@ cudaError_t pair_walk(const PairDev& d, int K, const uint8_t* x, uint8_t* out,
     uint32_t* counts = reinterpret_cast<uint32_t*>(entry + nb);
     uint32_t* offsets = counts + nb;
     uint8_t* flags = reinterpret_cast<uint8_t*>(offsets + nb);
-    const int tb = 128;
-    const int eb = int((nb + tb - 1) / tb);
     const int emit_ctas = int((nb + kWalkWarps - 1) / kWalkWarps);
     cudaError_t e = cudaMemsetAsync(flags, 0, size_t(M), stream);
     if (e != cudaSuccess) return e;
@@ -997,7 +1031,7 @@ cudaError_t pair_walk(const PairDev& d, int K, const uint8_t* x, uint8_t* out,
         emit<<<emit_ctas, 32 * kWalkWarps, 0, stream>>>(d, entry, flags, counts);
         mark(3);
         walk_scan_kernel<<<1, 1, 0, stream>>>(counts, nb, offsets, out_len);
-        walk_write_kernel<<<eb, tb, 0, stream>>>(x, M, flags, offsets, out);
+        walk_write_kernel<<<emit_ctas, 128, 0, stream>>>(x, M, flags, offsets, out);
         mark(4);
         if (dbg) {
             cudaEventSynchronize(ev[4]);
