@@ -39,11 +39,14 @@ constexpr int kWaveWarps = 4;       // warps per CTA (batch kernel)
 constexpr int kWaveTab = 32 * 256;     // per-warp match table bytes: [lane][byte] -> R-bit row mask
 
 
-// Steps of one band: lane l owns rows i0 + R l + r.  Prov(t, up, y) is
-// called by the whole warp at step t and sets, for lane 0 (column t), the top
-// boundary c[i0-1][t] (0 for the first band) and the column byte;
-// BottomFn(j, v) receives c[i0 + 32R - 1][j] from lane 31.  Returns, in every
-// lane, the final value of row `want_row` (0 if not in this band).
+// Steps of one band: lane l owns rows i0 + R l + r and, at step t, the two
+// columns 2(t - l) and 2(t - l) + 1 (two columns per step halve the per-step
+// work of the shuffle, the bounds tests and the boundary hand-off).
+// Prov(t, upA, yA, upB, yB) is called by the whole warp at step t and sets,
+// for lane 0 (columns 2t, 2t+1), the top boundary c[i0-1][.] (0 for the first
+// band) and the column bytes; BottomFn(j, v) receives c[i0 + 32R - 1][j] from
+// lane 31.  Returns, in every lane, the final value of row `want_row` (0 if
+// not in this band).
 template <typename Prov, typename BottomFn>
 __device__ __forceinline__ int32_t sweep_band(const uint8_t* rowp, int64_t i0, int64_t m,
                                               int64_t n, uint8_t* tab, Prov prov,
@@ -64,35 +67,49 @@ __device__ __forceinline__ int32_t sweep_band(const uint8_t* rowp, int64_t i0, i
 #pragma unroll
     for (int r = 0; r < kWaveR; ++r) left[r] = 0;
     int32_t prev_up = 0;  // c[top-1][j-1] of this lane's first row
-    uint32_t send = 0;
-    const int64_t T = n + 31;
-    for (int64_t t = 0; t < T; ++t) {
-        const uint32_t recv = __shfl_up_sync(kFullMask, send, 1);
-        const int64_t j = t - lane;
-        int32_t up0;
-        uint32_t y0;
-        prov(t, up0, y0);
-        const int32_t up = lane == 0 ? up0 : int32_t(recv >> 8);
-        const uint32_t y = lane == 0 ? y0 : (recv & 0xffu);
-        if (j >= 0 && j < n) {
-            // row r's match bit at bit 31 - r: each row shifts it into the
-            // carry flag, and diag + match is one add-with-carry
-            uint32_t mm = uint32_t(mt[y]) << 24;
-            int32_t u = up, dg = prev_up;
+    uint32_t sendA = 0, sendB = 0;
+    const int n2 = int((n + 1) >> 1);  // column pairs (n < 2^31)
+    const int T = n2 + 31;
+    // one column: 8 rows, each match bit shifted into the carry flag so that
+    // diag + match is one add-with-carry
+    auto column = [&](int32_t up, uint32_t y) {
+        uint32_t mm = uint32_t(mt[y]) << 24;
+        int32_t u = up, dg = prev_up;
 #pragma unroll
-            for (int r = 0; r < kWaveR; ++r) {
-                int32_t dm;
-                asm("{\n\tadd.cc.u32 %0, %0, %0;\n\taddc.u32 %1, %2, 0;\n\t}"
-                    : "+r"(mm), "=r"(dm)
-                    : "r"(dg));
-                const int32_t v = __vimax3_s32(u, left[r], dm);
-                dg = left[r];
-                left[r] = v;
-                u = v;
+        for (int r = 0; r < kWaveR; ++r) {
+            int32_t dm;
+            asm("{\n\tadd.cc.u32 %0, %0, %0;\n\taddc.u32 %1, %2, 0;\n\t}"
+                : "+r"(mm), "=r"(dm)
+                : "r"(dg));
+            const int32_t v = __vimax3_s32(u, left[r], dm);
+            dg = left[r];
+            left[r] = v;
+            u = v;
+        }
+        prev_up = up;
+        return u;
+    };
+    for (int t = 0; t < T; ++t) {
+        const uint32_t ra = __shfl_up_sync(kFullMask, sendA, 1);
+        const uint32_t rb = __shfl_up_sync(kFullMask, sendB, 1);
+        const int jp = t - lane;  // column pair
+        int32_t upA0, upB0;
+        uint32_t yA0, yB0;
+        prov(t, upA0, yA0, upB0, yB0);
+        const int32_t upA = lane == 0 ? upA0 : int32_t(ra >> 8);
+        const uint32_t yA = lane == 0 ? yA0 : (ra & 0xffu);
+        const int32_t upB = lane == 0 ? upB0 : int32_t(rb >> 8);
+        const uint32_t yB = lane == 0 ? yB0 : (rb & 0xffu);
+        if (unsigned(jp) < unsigned(n2)) {
+            const int64_t ja = 2 * int64_t(jp);
+            const int32_t ua = column(upA, yA);
+            sendA = (uint32_t(ua) << 8) | yA;
+            if (lane == 31) bottom(ja, ua);
+            if (ja + 1 < n) {  // false only for the last pair of an odd n
+                const int32_t ub = column(upB, yB);
+                sendB = (uint32_t(ub) << 8) | yB;
+                if (lane == 31) bottom(ja + 1, ub);
             }
-            prev_up = up;
-            send = (uint32_t(u) << 8) | y;
-            if (lane == 31) bottom(j, u);
         }
     }
     int32_t res = 0;
@@ -145,10 +162,13 @@ __global__ void __launch_bounds__(32 * kWaveWarps) wave_batch_kernel(WaveBatchDe
             const bool first = i0 == 0;
             const int32_t v = sweep_band(
                 rowp, i0, m, n, tab,
-                [&](int64_t t, int32_t& up, uint32_t& y) {
-                    const bool in = lane == 0 && t < n;
-                    up = (in && !first) ? bnd[t] : 0;
-                    y = in ? uint32_t(cs[t]) : 0u;
+                [&](int t, int32_t& upA, uint32_t& yA, int32_t& upB, uint32_t& yB) {
+                    const int64_t ja = 2 * int64_t(t);
+                    const bool ina = lane == 0 && ja < n, inb = lane == 0 && ja + 1 < n;
+                    upA = (ina && !first) ? bnd[ja] : 0;
+                    yA = ina ? uint32_t(cs[ja]) : 0u;
+                    upB = (inb && !first) ? bnd[ja + 1] : 0;
+                    yB = inb ? uint32_t(cs[ja + 1]) : 0u;
                 },
                 [&](int64_t j, int32_t v) { bnd[j] = v; }, m - 1);
             if (i0 + kWaveBand >= m) res = v;
@@ -201,21 +221,27 @@ __global__ void __launch_bounds__(32) wave_pair_kernel(WavePairDev d) {
         load_win(32, nw, nc);
         const int32_t v = sweep_band(
             d.rowp, i0, m, n, tab,
-            [&](int64_t t, int32_t& up, uint32_t& y) {
-                if ((t & 31) == 0 && t < n) {
-                    if (t > 0) {
+            [&](int t, int32_t& upA, uint32_t& yA, int32_t& upB, uint32_t& yB) {
+                const int64_t ja = 2 * int64_t(t);  // columns ja, ja + 1 (same window)
+                if ((ja & 31) == 0 && ja < n) {
+                    if (ja > 0) {
                         cw = nw;
                         cc = nc;
-                        load_win(t + 32, nw, nc);
+                        load_win(ja + 32, nw, nc);
                     }
                     // wait until band b-1 has published the whole window
                     while (__any_sync(kFullMask, (cw & 0xffu) != prev_tag))
-                        if ((cw & 0xffu) != prev_tag) cw = ld_relaxed(above + t + lane);
+                        if ((cw & 0xffu) != prev_tag) cw = ld_relaxed(above + ja + lane);
                 }
-                const uint32_t w = __shfl_sync(kFullMask, cw, int(t & 31));
-                const uint32_t c = __shfl_sync(kFullMask, cc, int(t & 31));
-                up = (first || t >= n) ? 0 : int32_t(w >> 8);
-                y = c;
+                const int la = int(ja & 31);
+                const uint32_t wa = __shfl_sync(kFullMask, cw, la);
+                const uint32_t ca = __shfl_sync(kFullMask, cc, la);
+                const uint32_t wb = __shfl_sync(kFullMask, cw, la + 1);
+                const uint32_t cb = __shfl_sync(kFullMask, cc, la + 1);
+                upA = (first || ja >= n) ? 0 : int32_t(wa >> 8);
+                yA = ca;
+                upB = (first || ja + 1 >= n) ? 0 : int32_t(wb >> 8);
+                yB = cb;
             },
             [&](int64_t j, int32_t val) {
                 if (!last) st_relaxed(below + j, (uint32_t(val) << 8) | my_tag);
