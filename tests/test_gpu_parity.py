@@ -421,6 +421,27 @@ def test_subsequence_shapes(wl, restatement, m, n):
     assert wl.lcs_subsequence(x, y) == restatement.subsequence(x, y)
 
 
+def test_subsequence_long_left_jumps(wl, restatement):
+    """Rows whose next match lies hundreds of columns to the left (the warp
+    walker's window is 96 columns: these take its serial row step), runs of
+    identical symbols, and blocks whose candidate walks never merge."""
+    rng = np.random.default_rng(97)
+    cases = [
+        (b"Z" * 3, b"Z" + b"A" * 3000),
+        (b"AB" * 400 + b"Z", b"Z" + b"C" * 5000 + b"AB" * 100),
+        (b"Q" + b"AC" * 2000, b"AC" * 100 + b"G" * 4000 + b"Q"),
+        (b"A" * 1500, b"A" * 700),
+        (b"A" * 700, b"A" * 1500),
+    ]
+    for _ in range(4):
+        m, n = int(rng.integers(300, 3000)), int(rng.integers(3000, 12000))
+        x = rng.choice(np.frombuffer(b"AC", np.uint8), m).tobytes()
+        y = rng.choice(np.frombuffer(b"ACGT" * 3 + b"NNNNNNNNNNNNNNNNNNNNNNNNN", np.uint8), n).tobytes()
+        cases.append((x, y))
+    for x, y in cases:
+        assert wl.lcs_subsequence(x, y) == restatement.subsequence(x, y), (len(x), len(y))
+
+
 def test_subsequence_byte_alphabet(wl, restatement):
     rng = np.random.default_rng(256)
     for m, n in [(3000, 2500), (700, 4000), (4000, 700)]:
