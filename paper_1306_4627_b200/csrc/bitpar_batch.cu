@@ -33,6 +33,13 @@ namespace wlcs {
 namespace {
 
 constexpr int kMaxK = 12;
+#ifdef WLCS_BATCH_TRACE
+// Diagnostic build only (tools/trace_probe.py): per task the globaltimer at
+// its start and end, smid << 32 | build ns, (16 S + K) << 32 | max rows.
+constexpr int kTraceMax = 1 << 15;
+__device__ unsigned long long g_trace[kTraceMax][4];
+__device__ unsigned int g_trace_n;
+#endif
 #ifndef WLCS_BATCH_HALF_UNROLL
 #define WLCS_BATCH_HALF_UNROLL 1
 #endif
@@ -670,12 +677,20 @@ __global__ void __launch_bounds__(32) batch_main_kernel(BatchDev d) {
         const bool active = idx < ti.last;
         const uint32_t pair = active ? d.vals[idx] : 0u;
         const LanePair p = lane_pair(d, active, pair);
+#ifdef WLCS_BATCH_TRACE
+        unsigned long long trb0;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(trb0));
+#endif
         uint32_t zrep = 0;
         if (build_task(d, p, K, s, sbase, &zrep) == 0u) {
             // Alphabet too large for this warp's shared-memory slice.
             if (active && s == 0) d.overflow[atomicAdd(d.meta + kMetaOverflow, 1u)] = pair;
             continue;
         }
+#ifdef WLCS_BATCH_TRACE
+        unsigned long long tr0;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr0));
+#endif
         int zeros = 0;
         switch ((S > 1 ? 16 : 0) + (K - 1)) {
             WLCS_SWEEP_CASE(0, 1) WLCS_SWEEP_CASE(0, 2) WLCS_SWEEP_CASE(0, 3)
@@ -691,6 +706,24 @@ __global__ void __launch_bounds__(32) batch_main_kernel(BatchDev d) {
         }
         for (int o = S >> 1; o >= 1; o >>= 1) zeros += __shfl_xor_sync(kFullMask, zeros, o);
         if (active && s == 0) d.out[pair] = uint32_t(zeros);
+#ifdef WLCS_BATCH_TRACE
+        {
+            unsigned long long tr1;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr1));
+            const int mr = warp_max(int(p.rows));
+            if (lane == 0) {
+                uint32_t smid;
+                asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+                const unsigned i = atomicAdd(&g_trace_n, 1u);
+                if (i < kTraceMax) {
+                    g_trace[i][0] = trb0;
+                    g_trace[i][1] = tr1;
+                    g_trace[i][2] = (uint64_t(smid) << 32) | uint32_t(tr0 - trb0);
+                    g_trace[i][3] = (uint64_t(S * 16 + K) << 32) | uint32_t(mr);
+                }
+            }
+        }
+#endif
     }
 }
 #undef WLCS_SWEEP_CASE
@@ -723,21 +756,51 @@ cudaError_t batch_launch(BatchDev d, void* workspace, int sms, cudaStream_t stre
         d, hist, bucket, rank);
     batch_scatter_kernel<<<int((d.pairs + kScatterPairs - 1) / kScatterPairs), 1024, 0, stream>>>(
         d, hist, bucket, rank);
-    int occ = 0;
+    // kernel attributes and the occupancy query once per (thread, device,
+    // smem size): fewer driver calls on every launch
+    thread_local int cached_dev = -1, cached_smem = -1, cached_occ = 0;
     const int smem = batch_smem_per_cta(d.pm_bytes);
-    e = cudaFuncSetAttribute(batch_main_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    int dev = 0;
+    e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(batch_main_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
-                             cudaSharedmemCarveoutMaxShared);
-    if (e != cudaSuccess) return e;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, batch_main_kernel, 32, smem);
-    if (e != cudaSuccess) return e;
-    if (occ < 1) occ = 1;
+    if (dev != cached_dev || smem != cached_smem) {
+        int occ = 0;
+        e = cudaFuncSetAttribute(batch_main_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 smem);
+        if (e != cudaSuccess) return e;
+        e = cudaFuncSetAttribute(batch_main_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                 cudaSharedmemCarveoutMaxShared);
+        if (e != cudaSuccess) return e;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, batch_main_kernel, 32, smem);
+        if (e != cudaSuccess) return e;
+        cached_dev = dev;
+        cached_smem = smem;
+        cached_occ = occ < 1 ? 1 : occ;
+    }
+    const int occ = cached_occ;
     if (ev_main0) cudaEventRecord(ev_main0, stream);
     batch_main_kernel<<<sms * occ, 32, smem, stream>>>(d);
     if (ev_main1) cudaEventRecord(ev_main1, stream);
     return cudaGetLastError();
 }
+
+#ifdef WLCS_BATCH_TRACE
+}  // namespace wlcs
+extern "C" int wlcs_debug_batch_trace(unsigned long long* out, unsigned int cap, int reset) {
+    unsigned int n = 0;
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(&n, wlcs::g_trace_n, 4);
+    if (n > unsigned(wlcs::kTraceMax)) n = wlcs::kTraceMax;
+    if (n > cap) n = cap;
+    if (out && n) cudaMemcpyFromSymbol(out, wlcs::g_trace, size_t(n) * 32);
+    if (reset) {
+        const unsigned int z = 0;
+        cudaMemcpyToSymbol(wlcs::g_trace_n, &z, 4);
+    }
+    return int(n);
+}
+namespace wlcs {
+#endif
 
 uint32_t* batch_overflow_count_ptr(void* workspace, uint32_t) {
     return static_cast<uint32_t*>(workspace) + kMetaOverflow;

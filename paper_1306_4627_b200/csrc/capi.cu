@@ -84,11 +84,16 @@ struct Ctx {
     cudaStream_t stream = nullptr;
     cudaStream_t copy_stream = nullptr;  // host batch pipeline: H2D of chunk k+1 || compute of k
     std::vector<cudaEvent_t> chunk_ev;
+    // pinned host words for the small D2H reads (counts, lengths) that end a
+    // call: a pageable destination would make each one a staged, synchronous
+    // copy (~10 us) inside the caller's timed region
+    uint64_t* hscratch = nullptr;
     // batch
     DevBuf xs, ys, xoff, yoff, out, ws, ws2;
     // single pair
     DevBuf px, py, pmg, carry, small, rows, outrev, codes, ry, vbuf, wave, sink, walk;
     ~Ctx() {
+        if (hscratch) cudaFreeHost(hscratch);
         for (cudaEvent_t e : chunk_ev) cudaEventDestroy(e);
         if (copy_stream) cudaStreamDestroy(copy_stream);
         if (stream) cudaStreamDestroy(stream);
@@ -127,6 +132,13 @@ int get_ctx(Ctx** out) {
     if (e != cudaSuccess) {
         delete c;
         return cuda_fail(e, "cudaStreamCreate");
+    }
+    e = cudaHostAlloc(reinterpret_cast<void**>(&c->hscratch), 64 * sizeof(uint64_t),
+                      cudaHostAllocDefault);
+    if (e != cudaSuccess) {
+        c->hscratch = nullptr;
+        delete c;
+        return cuda_fail(e, "cudaHostAlloc");
     }
     t_ctx.by_device[dev] = c;
     *out = c;
@@ -328,11 +340,10 @@ int pair_length_device(Ctx& c, const uint8_t* dx, size_t m, const uint8_t* dy, s
         WLCS_CUDA(wlcs::pair_split_combine(P.v_out, plan.d.prob[1].v_out, P.W, P.cols, scratch,
                                            zeros, c.stream));
     }
-    unsigned long long len = 0;
-    WLCS_CUDA(cudaMemcpyAsync(&len, zeros, 8, cudaMemcpyDeviceToHost, c.stream));
+    WLCS_CUDA(cudaMemcpyAsync(c.hscratch, zeros, 8, cudaMemcpyDeviceToHost, c.stream));
     WLCS_CUDA(cudaStreamSynchronize(c.stream));
     if (c.timing) WLCS_CUDA(cudaEventElapsedTime(&c.last_main_ms, c.ev0, c.ev1));
-    *out = uint32_t(len);
+    *out = uint32_t(c.hscratch[0]);
     return WLCS_OK;
 }
 
@@ -403,10 +414,11 @@ int batch_overflow_pass(Ctx& c, wlcs::BatchDev d, const uint32_t* list, uint32_t
     d.pm_bytes = 257 * 128;
     WLCS_CUDA(c.ws2.ensure(wlcs::batch_workspace_bytes(n, d.pm_bytes)));
     WLCS_CUDA(wlcs::batch_launch(d, c.ws2.p, c.sms, s));
-    uint32_t n2 = 0;
-    WLCS_CUDA(cudaMemcpyAsync(&n2, wlcs::batch_overflow_count_ptr(c.ws2.p, n), 4,
+    uint32_t* h2 = reinterpret_cast<uint32_t*>(c.hscratch + 1);
+    WLCS_CUDA(cudaMemcpyAsync(h2, wlcs::batch_overflow_count_ptr(c.ws2.p, n), 4,
                               cudaMemcpyDeviceToHost, s));
     WLCS_CUDA(cudaStreamSynchronize(s));
+    const uint32_t n2 = *h2;
     if (n2 == 0) return WLCS_OK;
     left.resize(n2);
     WLCS_CUDA(cudaMemcpy(left.data(), wlcs::batch_overflow_list_ptr(c.ws2.p, n), n2 * 4,
@@ -441,9 +453,10 @@ int batch_device(Ctx& c, const uint8_t* d_xs, const uint64_t* d_xoff, const uint
         if (c.timing) WLCS_CUDA(cudaEventRecord(c.ev0, stream));
         WLCS_CUDA(wlcs::wave_batch_launch(d, c.sms, stream));
         if (c.timing) WLCS_CUDA(cudaEventRecord(c.ev1, stream));
-        uint32_t overflow = 0;
-        WLCS_CUDA(cudaMemcpyAsync(&overflow, d.overflow_count, 4, cudaMemcpyDeviceToHost, stream));
+        uint32_t* hov = reinterpret_cast<uint32_t*>(c.hscratch);
+        WLCS_CUDA(cudaMemcpyAsync(hov, d.overflow_count, 4, cudaMemcpyDeviceToHost, stream));
         WLCS_CUDA(cudaStreamSynchronize(stream));
+        const uint32_t overflow = *hov;
         if (c.timing) WLCS_CUDA(cudaEventElapsedTime(&c.last_main_ms, c.ev0, c.ev1));
         if (overflow == 0) return WLCS_OK;
         std::vector<uint32_t> ids(overflow);
@@ -480,11 +493,11 @@ int batch_device(Ctx& c, const uint8_t* d_xs, const uint64_t* d_xoff, const uint
     }
     WLCS_CUDA(wlcs::batch_launch(d, c.ws.p, c.sms, stream, c.timing ? c.ev0 : nullptr,
                                  c.timing ? c.ev1 : nullptr));
-    uint32_t overflow = 0;
-    WLCS_CUDA(cudaMemcpyAsync(&overflow,
-                              wlcs::batch_overflow_count_ptr(c.ws.p, uint32_t(pairs)),
+    uint32_t* hov = reinterpret_cast<uint32_t*>(c.hscratch);
+    WLCS_CUDA(cudaMemcpyAsync(hov, wlcs::batch_overflow_count_ptr(c.ws.p, uint32_t(pairs)),
                               4, cudaMemcpyDeviceToHost, stream));
     WLCS_CUDA(cudaStreamSynchronize(stream));
+    const uint32_t overflow = *hov;
     if (c.timing) WLCS_CUDA(cudaEventElapsedTime(&c.last_main_ms, c.ev0, c.ev1));
     if (overflow == 0) return WLCS_OK;
     // Alphabet too large for the lane shape: second pass at one word per lane;
@@ -561,18 +574,20 @@ int batch_host_pipelined(Ctx& c, const uint8_t* xs, const uint64_t* x_off, const
                                      (c.timing && ends && k == nchunks - 1) ? c.ev1 : nullptr));
     }
     WLCS_CUDA(cudaMemcpyAsync(out, c.out.p, pairs * 4, cudaMemcpyDeviceToHost, s));
-    std::vector<uint32_t> ovf(nchunks, 0);
+    // per-chunk overflow counts into the pinned scratch (<= 64 chunks)
+    uint32_t* ovf = reinterpret_cast<uint32_t*>(c.hscratch);
     for (int k = 0; k < nchunks; ++k)
         WLCS_CUDA(cudaMemcpyAsync(&ovf[k],
                                   wlcs::batch_overflow_count_ptr(c.ws.as<uint8_t>() + ws_off[k],
                                                                  uint32_t(p0[k + 1] - p0[k])),
                                   4, cudaMemcpyDeviceToHost, s));
     WLCS_CUDA(cudaStreamSynchronize(s));
+    const std::vector<uint32_t> ovf_n(ovf, ovf + nchunks);  // the scratch is reused below
     if (c.timing) WLCS_CUDA(cudaEventElapsedTime(&c.last_main_ms, c.ev0, c.ev1));
     std::vector<std::vector<uint32_t>> left(nchunks);
     bool second = false;
     for (int k = 0; k < nchunks; ++k) {
-        if (!ovf[k]) continue;
+        if (!ovf_n[k]) continue;
         wlcs::BatchDev d{};
         d.xs = dxs;
         d.xoff = c.xoff.as<uint64_t>() + p0[k];
@@ -585,7 +600,7 @@ int batch_host_pipelined(Ctx& c, const uint8_t* xs, const uint64_t* x_off, const
                 c, d,
                 wlcs::batch_overflow_list_ptr(c.ws.as<uint8_t>() + ws_off[k],
                                               uint32_t(p0[k + 1] - p0[k])),
-                ovf[k], s, left[k]))
+                ovf_n[k], s, left[k]))
             return rc;
         second = true;
     }
@@ -712,10 +727,10 @@ int wlcs_subsequence(const uint8_t* x, size_t m, const uint8_t* y, size_t n,
     uint32_t* dmiss = reinterpret_cast<uint32_t*>(zeros_dev + 2);
     WLCS_CUDA(wlcs::pair_walk(plan.d, plan.K, dx, c->outrev.as<uint8_t>(), dlen, c->walk.p,
                               dmiss, c->stream));
-    unsigned long long len = 0, zeros = 0;
-    WLCS_CUDA(cudaMemcpyAsync(&len, dlen, 8, cudaMemcpyDeviceToHost, c->stream));
-    WLCS_CUDA(cudaMemcpyAsync(&zeros, zeros_dev, 8, cudaMemcpyDeviceToHost, c->stream));
+    WLCS_CUDA(cudaMemcpyAsync(c->hscratch, dlen, 8, cudaMemcpyDeviceToHost, c->stream));
+    WLCS_CUDA(cudaMemcpyAsync(c->hscratch + 1, zeros_dev, 8, cudaMemcpyDeviceToHost, c->stream));
     WLCS_CUDA(cudaStreamSynchronize(c->stream));
+    const unsigned long long len = c->hscratch[0], zeros = c->hscratch[1];
     if (c->timing) WLCS_CUDA(cudaEventElapsedTime(&c->last_main_ms, c->ev0, c->ev1));
     if (env_int("WLCS_DEBUG_WALK", 0)) {
         uint32_t miss[3] = {0, 0, 0};
@@ -769,7 +784,7 @@ int wlcs_length_batch_ex(const uint8_t* xs, const uint64_t* x_off, const uint8_t
     WLCS_CUDA(c->out.ensure(pairs * 4));
     cudaStream_t s = c->stream;
     const int nchunks = variant == WLCS_VARIANT_BITPARALLEL
-                            ? int(std::min<size_t>(size_t(env_int("WLCS_BATCH_CHUNKS", 4)),
+                            ? int(std::min<size_t>(std::min<size_t>(size_t(env_int("WLCS_BATCH_CHUNKS", 4)), 64),
                                                    pairs / 8192))
                             : 1;
     if (nchunks >= 2 && xs_bytes + ys_bytes >= (16u << 20))
