@@ -499,6 +499,14 @@ int batch_device(Ctx& c, const uint8_t* d_xs, const uint64_t* d_xoff, const uint
     WLCS_CUDA(cudaStreamSynchronize(stream));
     const uint32_t overflow = *hov;
     if (c.timing) WLCS_CUDA(cudaEventElapsedTime(&c.last_main_ms, c.ev0, c.ev1));
+    if (overflow && env_int("WLCS_DEBUG_BATCH", 0)) {
+        std::vector<uint32_t> ids(overflow);
+        WLCS_CUDA(cudaMemcpy(ids.data(), wlcs::batch_overflow_list_ptr(c.ws.p, uint32_t(pairs)),
+                             overflow * 4, cudaMemcpyDeviceToHost));
+        std::fprintf(stderr, "wlcs batch: %u pairs to the second pass:", overflow);
+        for (uint32_t i = 0; i < overflow && i < 16; ++i) std::fprintf(stderr, " %u", ids[i]);
+        std::fprintf(stderr, "\n");
+    }
     if (overflow == 0) return WLCS_OK;
     // Alphabet too large for the lane shape: second pass at one word per lane;
     // pairs too long for one warp: strip kernel.
