@@ -362,9 +362,9 @@ __device__ __forceinline__ uint32_t build_task(const BatchDev& d, const LanePair
     const uint32_t map = sbase;         // byte -> code
     const uint32_t inv = sbase + 256u;  // u16 low-nibble presence per high nibble
     const uint32_t pm = sbase + uint32_t(kMapBytes);
-    const bool wide = K > 4;
-    const uint32_t cs = wide ? 512u * uint32_t((K + 3) / 4) : 128u * uint32_t(K == 3 ? 4 : K);
-    const uint32_t ls = wide ? 16u : 4u * uint32_t(K == 3 ? 4 : K);
+    const bool wide = pm_slotted(K);
+    const uint32_t cs = wide ? 512u * uint32_t((K + 3) / 4) : 128u * pm_lane_words(K);
+    const uint32_t ls = wide ? 16u : 4u * pm_lane_words(K);
 
     // presence flags: one 32-bit word per byte value in the (not yet used) PM
     // region -- lanes marking the same byte hit the same word (no conflict)

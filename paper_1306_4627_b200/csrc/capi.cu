@@ -180,9 +180,16 @@ struct PairPlan {
 // lane pipeline + carry hand-off; tools/gpu/skew.sh); strips beyond the
 // resident warps run in waves; more resident strips than sub-partitions share
 // issue slots.
+// Lane shapes up to K = 10 words per lane in 26.25 KB of masks per warp
+// (21 codes x 1280 B: the 20-letter alphabet plus the zero row) -> 8 warps
+// per SM, two per sub-partition.
 int batch_kmax() {
-    const int k = env_int("WLCS_BATCH_KMAX", 12);
-    return k >= 1 && k <= 12 ? k : 12;
+    const int k = env_int("WLCS_BATCH_KMAX", 10);
+    return k >= 1 && k <= 12 ? k : 10;
+}
+int batch_pm_bytes() {  // >= flags + chunk stage; WLCS_BATCH_PM_KB overrides
+    const int kb = env_int("WLCS_BATCH_PM_KB", 0);
+    return kb > 0 ? std::max(kb, 14) * 1024 : 26880;
 }
 
 int choose_k(const Ctx& c, int64_t W, int64_t rows_per_prob, int sigma, int nprob) {
@@ -473,7 +480,7 @@ int batch_device(Ctx& c, const uint8_t* d_xs, const uint64_t* d_xoff, const uint
         }
         return WLCS_OK;
     }
-    const int pm_bytes = std::max(env_int("WLCS_BATCH_PM_KB", 33), 14) * 1024;  // >= flags + chunk stage
+    const int pm_bytes = batch_pm_bytes();
     const size_t ws_bytes = wlcs::batch_workspace_bytes(uint32_t(pairs), pm_bytes);
     WLCS_CUDA(c.ws.ensure(ws_bytes));
     wlcs::BatchDev d{};
@@ -541,7 +548,7 @@ int batch_host_pipelined(Ctx& c, const uint8_t* xs, const uint64_t* x_off, const
         WLCS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         c.chunk_ev.push_back(e);
     }
-    const int pm_bytes = std::max(env_int("WLCS_BATCH_PM_KB", 33), 14) * 1024;  // >= flags + chunk stage
+    const int pm_bytes = batch_pm_bytes();
     std::vector<size_t> p0(nchunks + 1);
     for (int k = 0; k <= nchunks; ++k) p0[k] = pairs * size_t(k) / size_t(nchunks);
     std::vector<size_t> ws_off(nchunks + 1, 0);

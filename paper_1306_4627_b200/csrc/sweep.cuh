@@ -9,7 +9,11 @@
 // Shared-memory match-mask layout, chosen so every warp-wide PM load is
 // bank-conflict free:
 //   K <= 4 : [code][lane][K words]               code stride 128*K bytes
-//   K  > 4 : [code][ceil(K/4) slot][lane][4 words] code stride 512*ceil(K/4)
+//   K 9-10 : [code][lane][10 words]              code stride 1280 bytes
+//            (40-byte lane stride: five LDS.64 per row, conflict-free; 17%
+//            less than the 3-slot layout, which lets kmax = 10 run 8 warps
+//            per SM in 26.25 KB of masks)
+//   other K > 4 : [code][ceil(K/4) slot][lane][4 words] code stride 512*ceil(K/4)
 #pragma once
 
 #include "rowstep.cuh"
@@ -17,12 +21,18 @@
 
 namespace wlcs {
 
+// Words per lane row of the non-slotted layouts (K = 3 and 9 are padded).
+__host__ __device__ constexpr uint32_t pm_lane_words(int K) {
+    return K == 3 ? 4u : (K == 9 || K == 10) ? 10u : uint32_t(K);
+}
+__host__ __device__ constexpr bool pm_slotted(int K) { return K > 4 && K != 9 && K != 10; }
+
 template <int K>
 struct PmLayout {
-    static constexpr int kWide = K > 4;
+    static constexpr int kWide = pm_slotted(K);
     static constexpr uint32_t code_stride =
-        kWide ? 512u * uint32_t((K + 3) / 4) : 128u * uint32_t(K == 3 ? 4 : K);
-    static constexpr uint32_t lane_stride = kWide ? 16u : 4u * uint32_t(K == 3 ? 4 : K);
+        kWide ? 512u * uint32_t((K + 3) / 4) : 128u * pm_lane_words(K);
+    static constexpr uint32_t lane_stride = kWide ? 16u : 4u * pm_lane_words(K);
     // byte offset of word k of `lane` inside one code row
     __device__ __forceinline__ static uint32_t word_offset(uint32_t lane, int k) {
         return kWide ? uint32_t(k >> 2) * 512u + lane * 16u + uint32_t(k & 3) * 4u
@@ -33,7 +43,17 @@ struct PmLayout {
 // Slot i (words 4i .. 4i+3) of a wide row sits at byte offset 512*i.
 template <int K>
 __device__ __forceinline__ void load_pm(const uint8_t* pm, uint32_t off, uint32_t* P) {
-    if constexpr (K >= 4) {
+    if constexpr (K == 9 || K == 10) {
+#pragma unroll
+        for (int i = 0; 2 * i < K; ++i) {
+            if (2 * i + 1 < K) {
+                const uint2 a = *reinterpret_cast<const uint2*>(pm + off + 8 * i);
+                P[2 * i] = a.x; P[2 * i + 1] = a.y;
+            } else {
+                P[2 * i] = *reinterpret_cast<const uint32_t*>(pm + off + 8 * i);
+            }
+        }
+    } else if constexpr (K >= 4) {
 #pragma unroll
         for (int i = 0; 4 * i < K; ++i) {
             const uint8_t* q = pm + off + 512 * i;
@@ -230,9 +250,25 @@ __device__ __forceinline__ void load_slot_sh(uint32_t a, uint32_t* P) {
 }
 
 // load_pm over a 32-bit shared address (same layouts as load_pm).
+template <int K, int I>
+__device__ __forceinline__ void load_pair_sh(uint32_t a, uint32_t* P) {
+    if constexpr (2 * I + 1 < K) {
+        const uint2 x = lds_v2<8 * I>(a);
+        P[2 * I] = x.x; P[2 * I + 1] = x.y;
+    } else if constexpr (2 * I < K) {
+        P[2 * I] = lds_u32<8 * I>(a);
+    }
+}
+
 template <int K>
 __device__ __forceinline__ void load_pm_sh(uint32_t a, uint32_t* P) {
-    if constexpr (K >= 4) {
+    if constexpr (K == 9 || K == 10) {
+        load_pair_sh<K, 0>(a, P);
+        load_pair_sh<K, 1>(a, P);
+        load_pair_sh<K, 2>(a, P);
+        load_pair_sh<K, 3>(a, P);
+        load_pair_sh<K, 4>(a, P);
+    } else if constexpr (K >= 4) {
         load_slot_sh<K, 0>(a, P);
         if constexpr (K > 4) load_slot_sh<K, 1>(a, P);
         if constexpr (K > 8) load_slot_sh<K, 2>(a, P);
