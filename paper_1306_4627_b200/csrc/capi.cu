@@ -6,6 +6,7 @@
 // CUDA is unusable every compute entry point fails with WLCS_E_NO_DEVICE.
 #include <algorithm>
 #include <cmath>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -143,6 +144,21 @@ int get_ctx(Ctx** out) {
     t_ctx.by_device[dev] = c;
     *out = c;
     return WLCS_OK;
+}
+
+// Waits for the end of a call's work on stream s.  A short bounded spin on
+// cudaStreamQuery returns within about a microsecond of completion (a
+// blocking or yielding cudaStreamSynchronize adds several to tens of
+// microseconds of wake-up to every synchronous call); long waits fall back to
+// the blocking synchronize.
+cudaError_t stream_wait(cudaStream_t s) {
+    const auto t0 = std::chrono::steady_clock::now();
+    for (;;) {
+        const cudaError_t e = cudaStreamQuery(s);
+        if (e != cudaErrorNotReady) return e;
+        if (std::chrono::steady_clock::now() - t0 > std::chrono::microseconds(3000))
+            return cudaStreamSynchronize(s);
+    }
 }
 
 int env_int(const char* name, int dflt) {
@@ -348,7 +364,7 @@ int pair_length_device(Ctx& c, const uint8_t* dx, size_t m, const uint8_t* dy, s
                                            zeros, c.stream));
     }
     WLCS_CUDA(cudaMemcpyAsync(c.hscratch, zeros, 8, cudaMemcpyDeviceToHost, c.stream));
-    WLCS_CUDA(cudaStreamSynchronize(c.stream));
+    WLCS_CUDA(stream_wait(c.stream));
     if (c.timing) WLCS_CUDA(cudaEventElapsedTime(&c.last_main_ms, c.ev0, c.ev1));
     *out = uint32_t(c.hscratch[0]);
     return WLCS_OK;
@@ -393,7 +409,7 @@ int pair_wave_device(Ctx& c, const uint8_t* dx, size_t m, const uint8_t* dy, siz
     WLCS_CUDA(wlcs::wave_pair_launch(d, c.sms, c.stream));
     if (c.timing) WLCS_CUDA(cudaEventRecord(c.ev1, c.stream));
     WLCS_CUDA(cudaMemcpyAsync(out, d.out, 4, cudaMemcpyDeviceToHost, c.stream));
-    WLCS_CUDA(cudaStreamSynchronize(c.stream));
+    WLCS_CUDA(stream_wait(c.stream));
     if (c.timing) WLCS_CUDA(cudaEventElapsedTime(&c.last_main_ms, c.ev0, c.ev1));
     return WLCS_OK;
 }
@@ -424,7 +440,7 @@ int batch_overflow_pass(Ctx& c, wlcs::BatchDev d, const uint32_t* list, uint32_t
     uint32_t* h2 = reinterpret_cast<uint32_t*>(c.hscratch + 1);
     WLCS_CUDA(cudaMemcpyAsync(h2, wlcs::batch_overflow_count_ptr(c.ws2.p, n), 4,
                               cudaMemcpyDeviceToHost, s));
-    WLCS_CUDA(cudaStreamSynchronize(s));
+    WLCS_CUDA(stream_wait(s));
     const uint32_t n2 = *h2;
     if (n2 == 0) return WLCS_OK;
     left.resize(n2);
@@ -462,7 +478,7 @@ int batch_device(Ctx& c, const uint8_t* d_xs, const uint64_t* d_xoff, const uint
         if (c.timing) WLCS_CUDA(cudaEventRecord(c.ev1, stream));
         uint32_t* hov = reinterpret_cast<uint32_t*>(c.hscratch);
         WLCS_CUDA(cudaMemcpyAsync(hov, d.overflow_count, 4, cudaMemcpyDeviceToHost, stream));
-        WLCS_CUDA(cudaStreamSynchronize(stream));
+        WLCS_CUDA(stream_wait(stream));
         const uint32_t overflow = *hov;
         if (c.timing) WLCS_CUDA(cudaEventElapsedTime(&c.last_main_ms, c.ev0, c.ev1));
         if (overflow == 0) return WLCS_OK;
@@ -503,7 +519,7 @@ int batch_device(Ctx& c, const uint8_t* d_xs, const uint64_t* d_xoff, const uint
     uint32_t* hov = reinterpret_cast<uint32_t*>(c.hscratch);
     WLCS_CUDA(cudaMemcpyAsync(hov, wlcs::batch_overflow_count_ptr(c.ws.p, uint32_t(pairs)),
                               4, cudaMemcpyDeviceToHost, stream));
-    WLCS_CUDA(cudaStreamSynchronize(stream));
+    WLCS_CUDA(stream_wait(stream));
     const uint32_t overflow = *hov;
     if (c.timing) WLCS_CUDA(cudaEventElapsedTime(&c.last_main_ms, c.ev0, c.ev1));
     if (overflow && env_int("WLCS_DEBUG_BATCH", 0)) {
@@ -596,7 +612,7 @@ int batch_host_pipelined(Ctx& c, const uint8_t* xs, const uint64_t* x_off, const
                                   wlcs::batch_overflow_count_ptr(c.ws.as<uint8_t>() + ws_off[k],
                                                                  uint32_t(p0[k + 1] - p0[k])),
                                   4, cudaMemcpyDeviceToHost, s));
-    WLCS_CUDA(cudaStreamSynchronize(s));
+    WLCS_CUDA(stream_wait(s));
     const std::vector<uint32_t> ovf_n(ovf, ovf + nchunks);  // the scratch is reused below
     if (c.timing) WLCS_CUDA(cudaEventElapsedTime(&c.last_main_ms, c.ev0, c.ev1));
     std::vector<std::vector<uint32_t>> left(nchunks);
@@ -744,7 +760,7 @@ int wlcs_subsequence(const uint8_t* x, size_t m, const uint8_t* y, size_t n,
                               dmiss, c->stream));
     WLCS_CUDA(cudaMemcpyAsync(c->hscratch, dlen, 8, cudaMemcpyDeviceToHost, c->stream));
     WLCS_CUDA(cudaMemcpyAsync(c->hscratch + 1, zeros_dev, 8, cudaMemcpyDeviceToHost, c->stream));
-    WLCS_CUDA(cudaStreamSynchronize(c->stream));
+    WLCS_CUDA(stream_wait(c->stream));
     const unsigned long long len = c->hscratch[0], zeros = c->hscratch[1];
     if (c->timing) WLCS_CUDA(cudaEventElapsedTime(&c->last_main_ms, c->ev0, c->ev1));
     if (env_int("WLCS_DEBUG_WALK", 0)) {
@@ -813,7 +829,7 @@ int wlcs_length_batch_ex(const uint8_t* xs, const uint64_t* x_off, const uint8_t
                       c->out.as<uint32_t>(), s);
     if (rc) return rc;
     WLCS_CUDA(cudaMemcpyAsync(out, c->out.p, pairs * 4, cudaMemcpyDeviceToHost, s));
-    WLCS_CUDA(cudaStreamSynchronize(s));
+    WLCS_CUDA(stream_wait(s));
     return WLCS_OK;
 }
 
@@ -1002,7 +1018,7 @@ int wlcs_colsplit_fill(const uint8_t* x, size_t m, const uint8_t* y, size_t n, s
     if (want[1] && v_rev)
         WLCS_CUDA(cudaMemcpyAsync(v_rev, c->vbuf.as<uint32_t>() + W, size_t(W) * 4,
                                   cudaMemcpyDeviceToHost, c->stream));
-    WLCS_CUDA(cudaStreamSynchronize(c->stream));
+    WLCS_CUDA(stream_wait(c->stream));
     if (c->timing) WLCS_CUDA(cudaEventElapsedTime(&c->last_main_ms, c->ev0, c->ev1));
     return WLCS_OK;
 }
@@ -1222,7 +1238,7 @@ int wlcs_fill_tables(const uint8_t* x, size_t m, const uint8_t* y, size_t n,
                                 c->stream));
     WLCS_CUDA(cudaMemcpyAsync(dp, tdp.p, dp_bytes, cudaMemcpyDeviceToHost, c->stream));
     WLCS_CUDA(cudaMemcpyAsync(back, tback.p, back_bytes, cudaMemcpyDeviceToHost, c->stream));
-    WLCS_CUDA(cudaStreamSynchronize(c->stream));
+    WLCS_CUDA(stream_wait(c->stream));
     return WLCS_OK;
 }
 
