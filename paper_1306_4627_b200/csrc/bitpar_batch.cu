@@ -67,6 +67,23 @@ constexpr size_t kWsPairs = kWsCursor + kBuckets;
 
 __device__ __forceinline__ int class_of(int sidx, int k) { return sidx * kMaxK + (k - 1); }
 
+// Queue order of the lane-shape classes: decreasing K (words per lane: a
+// task's duration is about K x its rows, whatever its S), then decreasing S
+// -- the longest tasks first, and one sweep variant hot in the I-cache at a
+// time (S = 2 and S = 4 share the chain variant of a K).  Pairs of 5-8 words
+// take the S = 2, K <= 4 shape (half-length tasks) so the queue ends short.
+#ifndef WLCS_BATCH_FINE_TAIL
+#define WLCS_BATCH_FINE_TAIL 1
+#endif
+__device__ __forceinline__ int order_of_class(int c) {
+    const int k = c % kMaxK + 1, sidx = c / kMaxK;
+    return (kMaxK - k) * 6 + (5 - sidx);
+}
+__device__ __forceinline__ int class_of_order(int o) {
+    const int k = kMaxK - o / 6, sidx = 5 - o % 6;
+    return class_of(sidx, k);
+}
+
 // One thread per pair.  Besides the bucket it records the pair's rank inside
 // its bucket: a block-local rank (shared-memory atomics) plus the block's base
 // in that bucket (one global atomic per block and bucket), so the scatter
@@ -100,9 +117,10 @@ __global__ void __launch_bounds__(kPlanThreads) batch_plan_kernel(BatchDev d, ui
             } else {
                 int sidx = 0;
                 while ((kmax << sidx) < w) ++sidx;
+                if (WLCS_BATCH_FINE_TAIL && sidx == 0 && w >= 5 && w <= 8) sidx = 1;
                 const int s = 1 << sidx;
                 const int k = int((w + s - 1) / s);
-                const int order = kNumClasses - 1 - class_of(sidx, k);
+                const int order = order_of_class(class_of(sidx, k));
                 uint64_t nch = (rows + 15) / 16;
                 if (nch > kChunkBuckets - 1) nch = kChunkBuckets - 1;
                 b = uint32_t(order * kChunkBuckets + (kChunkBuckets - 1 - int(nch)));
@@ -178,7 +196,7 @@ __device__ __forceinline__ void scan_buckets(const BatchDev& d, const uint32_t* 
             const int o = lane * kTableSlots + q;
             nt[q] = 0;
             if (o < kNumClasses) {
-                const uint32_t per_task = 32u >> ((kNumClasses - 1 - o) / kMaxK);
+                const uint32_t per_task = 32u >> (class_of_order(o) / kMaxK);
                 const uint32_t cnt = order_start[o + 1] - order_start[o];
                 d.meta[kMetaCount + o] = cnt;
                 d.meta[kMetaPairStart + o] = order_start[o];
@@ -288,7 +306,7 @@ __device__ __forceinline__ TaskInfo decode_task(const TaskTable& tt, uint32_t t)
     const uint32_t ts = __shfl_sync(kFullMask, slot == 0 ? tt.ts[0] : slot == 1 ? tt.ts[1] : tt.ts[2], src);
     const uint32_t ps = __shfl_sync(kFullMask, slot == 0 ? tt.ps[0] : slot == 1 ? tt.ps[1] : tt.ps[2], src);
     const uint32_t cn = __shfl_sync(kFullMask, slot == 0 ? tt.cn[0] : slot == 1 ? tt.cn[1] : tt.cn[2], src);
-    const int c = kNumClasses - 1 - order;
+    const int c = class_of_order(order);
     TaskInfo ti;
     ti.sidx = c / kMaxK;
     ti.K = c % kMaxK + 1;
