@@ -75,6 +75,9 @@ __device__ __forceinline__ int class_of(int sidx, int k) { return sidx * kMaxK +
 #ifndef WLCS_BATCH_FINE_TAIL
 #define WLCS_BATCH_FINE_TAIL 1
 #endif
+#ifndef WLCS_BATCH_FINE_MAXW
+#define WLCS_BATCH_FINE_MAXW 8
+#endif
 __device__ __forceinline__ int order_of_class(int c) {
     const int k = c % kMaxK + 1, sidx = c / kMaxK;
     return (kMaxK - k) * 6 + (5 - sidx);
@@ -117,7 +120,7 @@ __global__ void __launch_bounds__(kPlanThreads) batch_plan_kernel(BatchDev d, ui
             } else {
                 int sidx = 0;
                 while ((kmax << sidx) < w) ++sidx;
-                if (WLCS_BATCH_FINE_TAIL && sidx == 0 && w >= 5 && w <= 8) sidx = 1;
+                if (WLCS_BATCH_FINE_TAIL && sidx == 0 && w >= 5 && w <= WLCS_BATCH_FINE_MAXW) sidx = 1;
                 const int s = 1 << sidx;
                 const int k = int((w + s - 1) / s);
                 const int order = order_of_class(class_of(sidx, k));
