@@ -1,0 +1,5 @@
+for r in 1 2; do for v in "WLCS_LIB_PATH=tools/exp/base.so" "WLCS_LIB_PATH=tools/exp/sasc.so" "WLCS_BATCH_KMAX=12 WLCS_BATCH_PM_KB=33" "WLCS_BATCH_KMAX=8 WLCS_BATCH_PM_KB=22"; do
+env $v timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/ab.json 2>gpurun_out/ab.err
+python3 -c "
+import json;d=json.loads(open('gpurun_out/ab.json').read().strip().splitlines()[-1]);print('[$v]',d['ms_per_step'],d['roofline']['kernel_ms'],d['value'])"
+done; done
