@@ -368,8 +368,9 @@ def run_c2(args, dist):
                    "global_batch": args.pairs * dist.world, "seq_len": "200-1000",
                    "parallelism": f"pair-sharded x{dist.world} (no collective)",
                    "cells_per_gpu_step": cells, "l2": "flushed between steps (300 MB write)"},
-        # bit-parallel: plan, scan, scatter, main (CUB-free); wavefront: one kernel
-        "gpu_launches": (1 if wave else 4) * args.steps,
+        # bit-parallel: plan, scatter (with the bucket scan), main -- the
+        # workspace memset is a driver memset, not counted; wavefront: one kernel
+        "gpu_launches": (1 if wave else 3) * args.steps,
         "variant": args.variant,
         "roofline": {"bound": "int", "achieved": round(achieved, 3), "peak": round(peak_t, 3),
                      "unit": "Tops/s (int32 ALU, 3 ops per cell)" if wave else
