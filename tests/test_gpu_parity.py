@@ -492,3 +492,28 @@ def test_batch_many_tiny_pairs(wl, restatement):
     got = wl.lcs_length_batch(xb, xo, yb, yo)
     want = restatement.length_batch(np.frombuffer(xb, np.uint8), xo, np.frombuffer(yb, np.uint8), yo)
     assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("alphabet", [DNA, PROTEIN, bytes(range(7, 47))])
+def test_batch_every_lane_shape(wl, restatement, alphabet):
+    # The batch planner picks, from the shorter string's word count W, a lane
+    # shape (S lanes x K words, K <= 10), a mask layout (K <= 4, the 10-word
+    # rows of K = 9-10, or 4-word slots) and, for W = 5-8, the half-length
+    # S = 2 shape queued last.  Every W from 1 to 40 words at both ends of
+    # its 32-column range, as the x and as the y string, with row strings
+    # from 1 byte to well past the column string, plus a skewed mix.
+    rng = np.random.default_rng(20261020)
+    a = np.frombuffer(alphabet, dtype=np.uint8)
+    xs, ys = [], []
+    for w in range(1, 41):
+        for cols in (32 * w - 31, 32 * w):
+            for rows in (1, 15, 17, cols, cols + 1, 3 * cols + 5):
+                rows = max(rows, cols)  # the column string is the shorter one
+                c = a[rng.integers(0, len(a), cols)].tobytes()
+                r = a[rng.integers(0, len(a), rows)].tobytes()
+                if rng.integers(0, 2):
+                    xs.append(c); ys.append(r)
+                else:
+                    xs.append(r); ys.append(c)
+    xr, yr = rand_pairs(rng, 1500, 1, 1400, alphabet)
+    check_batch(wl, restatement, xs + xr, ys + yr)
