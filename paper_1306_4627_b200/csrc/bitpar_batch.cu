@@ -33,6 +33,9 @@ namespace wlcs {
 namespace {
 
 constexpr int kMaxK = 12;
+#ifndef WLCS_BATCH_BUILD2
+#define WLCS_BATCH_BUILD2 1
+#endif
 #ifdef WLCS_BATCH_TRACE
 // Diagnostic build only (tools/trace_probe.py): per task the globaltimer at
 // its start and end, smid << 32 | build ns, (16 S + K) << 32 | max rows.
@@ -516,6 +519,68 @@ __device__ __forceinline__ uint32_t build_task(const BatchDev& d, const LanePair
     const uint32_t lane_off = wide ? lane * 16u : lane * ls;
     const bool use_stage = sigma * cs <= uint32_t(d.pm_bytes) - uint32_t(nchk) * 512u;
     auto chunk2 = [&](int i) { return use_stage ? staged(i) : chunk(i); };
+#if WLCS_BATCH_BUILD2
+    // two words per iteration: their bit-plane transposes are independent
+    // (twice the instruction-level parallelism of this latency-bound phase)
+    auto woff_of = [&](int k) {
+        return lane_off + (wide ? uint32_t((k >> 2) * 512 + (k & 3) * 4) : uint32_t(k * 4));
+    };
+    {
+        uint4 c0v = chunk2(0), c1v = chunk2(1), c2v = chunk2(2), c3v = chunk2(3), c4v = chunk2(4);
+#pragma unroll 1
+        for (int k = 0; k < K; k += 2) {
+            const uint4 n1 = chunk2(2 * k + 5), n2 = chunk2(2 * k + 6), n3 = chunk2(2 * k + 7),
+                        n4 = chunk2(2 * k + 8);
+            uint32_t w0[8], w1[8], P0[8], P1[8];
+            word_bytes(c0v, c1v, c2v, q, fs, w0);
+            word_bytes(c2v, c3v, c4v, q, fs, w1);
+            bit_planes(w0, P0);
+            bit_planes(w1, P1);
+            const bool has1 = k + 1 < K;  // warp-uniform
+            const int nv0 = min(max(clen - 32 * k, 0), 32);
+            const int nv1 = has1 ? min(max(clen - 32 * (k + 1), 0), 32) : 0;
+            const uint32_t vm0 = nv0 >= 32 ? 0xffffffffu : ((1u << nv0) - 1u);
+            const uint32_t vm1 = nv1 >= 32 ? 0xffffffffu : ((1u << nv1) - 1u);
+            uint32_t ca0 = pm + woff_of(k), ca1 = pm + woff_of(k + 1);
+            sts_u32(ca0, 0u);  // code 0: the zero row
+            if (has1) sts_u32(ca1, 0u);
+            const uint32_t a0[4] = {~(P0[0] | P0[1]), P0[0] & ~P0[1], ~P0[0] & P0[1], P0[0] & P0[1]};
+            const uint32_t b0[4] = {~(P0[2] | P0[3]), P0[2] & ~P0[3], ~P0[2] & P0[3], P0[2] & P0[3]};
+            const uint32_t a1[4] = {~(P1[0] | P1[1]), P1[0] & ~P1[1], ~P1[0] & P1[1], P1[0] & P1[1]};
+            const uint32_t b1[4] = {~(P1[2] | P1[3]), P1[2] & ~P1[3], ~P1[2] & P1[3], P1[2] & P1[3]};
+            uint32_t groups = hm;
+            while (groups) {  // warp-uniform
+                const uint32_t h = uint32_t(__ffs(groups) - 1) >> 1;
+                groups &= groups - 1u;
+                const uint32_t m4 = 0u - (h & 1u), m5 = 0u - ((h >> 1) & 1u),
+                               m6 = 0u - ((h >> 2) & 1u), m7 = 0u - ((h >> 3) & 1u);
+                const uint32_t hi0 = vm0 & ~((P0[4] ^ m4) | (P0[5] ^ m5) | (P0[6] ^ m6) | (P0[7] ^ m7));
+                const uint32_t hi1 = vm1 & ~((P1[4] ^ m4) | (P1[5] ^ m5) | (P1[6] ^ m6) | (P1[7] ^ m7));
+                const uint32_t nm = lds_u16(inv + 2u * h);
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj) {
+                    if ((nm >> (4 * jj)) & 0xfu) {
+                        const uint32_t hb0 = hi0 & b0[jj], hb1 = hi1 & b1[jj];
+#pragma unroll
+                        for (int ii = 0; ii < 4; ++ii) {
+                            if ((nm >> (4 * jj + ii)) & 1u) {
+                                ca0 += cs;
+                                ca1 += cs;
+                                sts_u32(ca0, hb0 & a0[ii]);
+                                if (has1) sts_u32(ca1, hb1 & a1[ii]);
+                            }
+                        }
+                    }
+                }
+            }
+            c0v = c4v;
+            c1v = n1;
+            c2v = n2;
+            c3v = n3;
+            c4v = n4;
+        }
+    }
+#else
     {
         uint4 c0v = chunk2(0), c1v = chunk2(1), c2v = chunk2(2);
 #pragma unroll 1
@@ -564,6 +629,7 @@ __device__ __forceinline__ uint32_t build_task(const BatchDev& d, const LanePair
             c2v = n2;
         }
     }
+#endif
     __syncwarp();
     // the inverse table is done: zero it for the sweep (the all-zero map of
     // chunks outside a row string)
