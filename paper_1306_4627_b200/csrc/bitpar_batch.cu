@@ -10,10 +10,13 @@
 //  * plan:   one thread per pair picks the roles (the shorter string becomes
 //            the bit-vector "column" string -- LCS length is symmetric,
 //            SPEC.md:82), its word count W = ceil(cols/32) and a lane shape
-//            (S lanes per pair, K <= 12 words per lane, S*K >= W).  A counting
-//            sort (plan -> scan -> scatter) groups pairs by shape and, inside
-//            a shape, by decreasing 16-row chunk count, so the pairs of one
-//            warp task end on the same step.
+//            (S lanes per pair, K <= kmax words per lane -- 10 by default --,
+//            S*K >= W; 5-8 word pairs take S = 2).  A counting sort (plan ->
+//            scatter, which also scans the bucket counts) groups pairs by
+//            shape in queue order -- decreasing K, then S: the longest tasks
+//            first, half-length ones last -- and, inside a shape, by
+//            decreasing 16-row chunk count, so the pairs of one warp task end
+//            on the same step.
 //  * main:   persistent 1-warp CTAs pull tasks (32/S pairs of one shape) from
 //            an atomic counter.  Per task the warp builds, in shared memory, a
 //            byte->code map of the task's column alphabet and the match masks
