@@ -101,17 +101,23 @@ int wlcs_length_batch(const uint8_t* xs, const uint64_t* x_off, const uint8_t* y
 int wlcs_length_batch_ex(const uint8_t* xs, const uint64_t* x_off, const uint8_t* ys,
                          const uint64_t* y_off, size_t pairs, int variant, uint32_t* out);
 
-/* Batch on DEVICE pointers already resident in HBM (current device), enqueued
- * on `stream` (a cudaStream_t, NULL = the library's per-thread stream).  The
- * call returns after the results are written to d_out (it synchronises the
- * stream once to collect pairs that need the single-pair path).  d_xs and
- * d_ys must be 16-byte aligned (cudaMalloc / torch allocations are). */
+/* Batch on DEVICE pointers already resident in HBM (current device),
+ * ASYNCHRONOUS: the whole batch is enqueued on `stream` (a cudaStream_t; NULL
+ * = the legacy default stream, e.g. torch's default stream) and the call
+ * returns without waiting -- d_out is valid once the stream's work up to this
+ * point has completed.  No host round trip: pairs the first pass cannot hold
+ * (alphabet over its mask budget, or wider than its lane shapes) are finished
+ * by a second pass whose length is read on the device.  d_xs and d_ys must be
+ * 16-byte aligned (cudaMalloc / torch allocations are); each pair's strings
+ * must lie inside [d_xs, d_xs + xs_bytes) / [d_ys, d_ys + ys_bytes). */
 int wlcs_length_batch_device(const uint8_t* d_xs, const uint64_t* d_x_off, const uint8_t* d_ys,
                              const uint64_t* d_y_off, size_t pairs, uint64_t xs_bytes,
                              uint64_t ys_bytes, int variant, uint32_t* d_out, void* stream);
 
 /* Single pair on DEVICE pointers (length only; budget not applied; 16-byte
- * aligned buffers). */
+ * aligned buffers).  The fill is ordered after the work enqueued on `stream`
+ * (NULL = the legacy default stream) before the call; synchronous: *out is
+ * valid on return. */
 int wlcs_length_device(const uint8_t* d_x, size_t m, const uint8_t* d_y, size_t n, int variant,
                        uint32_t* out, void* stream);
 
@@ -203,6 +209,15 @@ int wlcs_length_batch_multi(const uint8_t* xs, const uint64_t* x_off, const uint
                             const uint64_t* y_off, size_t pairs, int n_gpus, uint32_t* out);
 int wlcs_length_strips(const uint8_t* x, size_t m, const uint8_t* y, size_t n, int n_gpus,
                        uint32_t* out);
+
+/* The column split of ONE device's pair played as `slices` ranks inside a
+ * single strip-kernel launch (2 * slices problems, one CTA pool each; slice
+ * g's first strips poll inboxes that slices g-1 / g+1 fill while running --
+ * the same fused hand-off as wlcs_colsplit_fill between GPUs).  max_ctas > 0
+ * caps the grid (tests: fewer warps per pool than strips per problem);
+ * slices <= 4.  x = rows, y = the split column string.  *out = LCS length. */
+int wlcs_colsplit_emulate(const uint8_t* x, size_t m, const uint8_t* y, size_t n, int slices,
+                          int max_ctas, uint32_t* out);
 
 /* Device memory helpers for the inboxes (current device). */
 int wlcs_device_alloc(size_t bytes, void** d_ptr); /* zero-filled */

@@ -64,6 +64,8 @@ class Restatement:
         lib.orc_length_cells.argtypes = [_u8p, _sz, _u8p, _sz]
         lib.orc_length_bitpar.restype = ctypes.c_uint32
         lib.orc_length_bitpar.argtypes = [_u8p, _sz, _u8p, _sz]
+        lib.orc_length_cells_mt.restype = ctypes.c_uint32
+        lib.orc_length_cells_mt.argtypes = [_u8p, _sz, _u8p, _sz, ctypes.c_int]
         lib.orc_fill_tables.restype = None
         lib.orc_fill_tables.argtypes = [_u8p, _sz, _u8p, _sz, _u32p, _u8p]
         lib.orc_traceback.restype = _sz
@@ -81,6 +83,9 @@ class Restatement:
         lib.orc_strip_zeros.restype = ctypes.c_uint64
         lib.orc_strip_zeros.argtypes = [_u64p, _sz]
         lib.orc_length_batch.restype = None
+        lib.orc_generate_pairs.restype = None
+        lib.orc_generate_pairs.argtypes = [_sz, _sz, _sz, _u8p, _sz, ctypes.c_uint64, _u8p, _u64p,
+                                           _u8p, _u64p]
         lib.orc_length_batch.argtypes = [_u8p, _u64p, _u8p, _u64p, _sz, _u32p]
         self.lib = lib
 
@@ -88,6 +93,13 @@ class Restatement:
         xa, xp, m = _buf(x)
         ya, yp, n = _buf(y)
         return int(self.lib.orc_length_cells(xp, m, yp, n))
+
+    def length_cells_mt(self, x, y, threads: int = 0) -> int:
+        """Two-row lcs_cell loop over column strips on `threads` host threads
+        (SURVEY.md 8(c) check (i) at full size)."""
+        xa, xp, m = _buf(x)
+        ya, yp, n = _buf(y)
+        return int(self.lib.orc_length_cells_mt(xp, m, yp, n, threads or (os.cpu_count() or 1)))
 
     def length_bitpar(self, x, y) -> int:
         xa, xp, m = _buf(x)
@@ -145,6 +157,19 @@ class Restatement:
         out = np.empty(max(1, length), dtype=np.uint8)
         self.lib.orc_generate_random(length, ap, alen, seed & (2**64 - 1), out.ctypes.data_as(_u8p))
         return out[:length].tobytes()
+
+    def generate_pairs(self, pairs: int, lo: int, hi: int, alphabet, seed: int):
+        """The C2 batch procedure (master MT19937-64 -> per-pair lengths and
+        seeds -> generate_random); returns (xs, x_off, ys, y_off) numpy arrays."""
+        aa, ap, alen = _buf(alphabet)
+        xs = np.empty(max(1, pairs * hi), np.uint8)
+        ys = np.empty(max(1, pairs * hi), np.uint8)
+        xo = np.empty(pairs + 1, np.uint64)
+        yo = np.empty(pairs + 1, np.uint64)
+        self.lib.orc_generate_pairs(pairs, lo, hi, ap, alen, seed & (2**64 - 1),
+                                    xs.ctypes.data_as(_u8p), xo.ctypes.data_as(_u64p),
+                                    ys.ctypes.data_as(_u8p), yo.ctypes.data_as(_u64p))
+        return xs, xo, ys, yo
 
     def strip_rows(self, x, ystrip, V: np.ndarray, carry_in: np.ndarray | None):
         """Rows of x over one column strip; V (uint64, ceil(ns/64)) updated in

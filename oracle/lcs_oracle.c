@@ -356,3 +356,137 @@ void orc_strip_rows(const uint8_t* x, size_t rows, const uint8_t* ystrip, size_t
 
 /* zero bits of V below ns (the strip's contribution to the LCS length) */
 uint64_t orc_strip_zeros(const uint64_t* V, size_t ns) { return zeros_in_prefix(V, ns); }
+
+/* ---------------------------------------------------------------------
+ * Full-size check (i) of SURVEY.md 8(c): the two-row lcs_cell loop of
+ * orc_length_cells (kernels_scalar.cpp:6-16 + cell.hpp:30-38, values only)
+ * spread over `threads` column strips so that 1e12-cell configurations (C4,
+ * C5) finish in minutes.  Strip t keeps its own row segment; for every row it
+ * needs the left neighbour's value in column lo_t - 1 of this row (left) and
+ * of the previous row (diag), which strip t-1 publishes in edge[t-1][i]
+ * followed by a release store of its row counter.  Same arithmetic as the
+ * one-thread loop; only the order in which independent cells are visited
+ * changes.  Returns UINT32_MAX on allocation failure.
+ * ------------------------------------------------------------------- */
+#include <pthread.h>
+#include <stdatomic.h>
+#include <sched.h>
+
+typedef struct {
+    const uint8_t* x;
+    size_t m;
+    const uint8_t* y;
+    size_t lo, hi;            /* columns [lo, hi), 1-based j = lo+1 .. hi */
+    uint32_t* edge_in;        /* left strip's last column per row, NULL for t = 0 */
+    _Atomic size_t* ready_in; /* rows published by the left strip */
+    uint32_t* edge_out;       /* this strip's last column per row (m + 1) */
+    _Atomic size_t* ready_out;
+    uint32_t last;
+} cells_strip_t;
+
+#define CELLS_PUBLISH_ROWS 256
+
+static void* cells_strip_main(void* arg) {
+    cells_strip_t* s = (cells_strip_t*)arg;
+    const size_t w = s->hi - s->lo;
+    uint32_t* row = (uint32_t*)calloc(w + 1, sizeof(uint32_t)); /* row[0] = column lo */
+    if (!row) {
+        s->last = UINT32_MAX;
+        return NULL;
+    }
+    const uint8_t* ys = s->y + s->lo;
+    size_t avail = 0;
+    for (size_t i = 1; i <= s->m; ++i) {
+        if (s->edge_in) {
+            while (avail < i) {
+                avail = atomic_load_explicit(s->ready_in, memory_order_acquire);
+                if (avail < i) sched_yield();
+            }
+        }
+        const uint8_t xi = s->x[i - 1];
+        uint32_t diag = row[0];                          /* c[i-1][lo] */
+        uint32_t left = s->edge_in ? s->edge_in[i] : 0u; /* c[i][lo]   */
+        row[0] = left;
+        for (size_t k = 1; k <= w; ++k) {
+            const uint32_t up = row[k];
+            uint8_t a;
+            left = cell_value(xi, ys[k - 1], diag, up, left, &a);
+            diag = up;
+            row[k] = left;
+        }
+        s->edge_out[i] = row[w];
+        if ((i % CELLS_PUBLISH_ROWS) == 0 || i == s->m)
+            atomic_store_explicit(s->ready_out, i, memory_order_release);
+    }
+    s->last = row[w];
+    free(row);
+    return NULL;
+}
+
+uint32_t orc_length_cells_mt(const uint8_t* x, size_t m, const uint8_t* y, size_t n,
+                             int threads) {
+    if (m == 0 || n == 0) return 0;
+    if (threads < 1) threads = 1;
+    if ((size_t)threads > n) threads = (int)n;
+    cells_strip_t* st = (cells_strip_t*)calloc((size_t)threads, sizeof(cells_strip_t));
+    uint32_t* edges = (uint32_t*)calloc((size_t)threads * (m + 1), sizeof(uint32_t));
+    _Atomic size_t* ready = (_Atomic size_t*)calloc((size_t)threads, sizeof(_Atomic size_t));
+    pthread_t* tid = (pthread_t*)calloc((size_t)threads, sizeof(pthread_t));
+    if (!st || !edges || !ready || !tid) {
+        free(st);
+        free(edges);
+        free((void*)ready);
+        free(tid);
+        return UINT32_MAX;
+    }
+    for (int t = 0; t < threads; ++t) {
+        st[t].x = x;
+        st[t].m = m;
+        st[t].y = y;
+        st[t].lo = n * (size_t)t / (size_t)threads;
+        st[t].hi = n * (size_t)(t + 1) / (size_t)threads;
+        st[t].edge_in = t ? edges + (size_t)(t - 1) * (m + 1) : NULL;
+        st[t].ready_in = t ? &ready[t - 1] : NULL;
+        st[t].edge_out = edges + (size_t)t * (m + 1);
+        st[t].ready_out = &ready[t];
+        atomic_init(&ready[t], 0);
+    }
+    for (int t = 0; t < threads; ++t) pthread_create(&tid[t], NULL, cells_strip_main, &st[t]);
+    for (int t = 0; t < threads; ++t) pthread_join(tid[t], NULL);
+    uint32_t r = st[threads - 1].last;
+    for (int t = 0; t < threads; ++t)
+        if (st[t].last == UINT32_MAX) r = UINT32_MAX;
+    free(st);
+    free(edges);
+    free((void*)ready);
+    free(tid);
+    return r;
+}
+
+/* The C2 batch generator of bench.py / tests, restated on the oracle side so
+ * that the reference arm never loads the product library: master =
+ * std::mt19937_64(seed); per pair m = lo + master() % (hi - lo + 1), n
+ * likewise, then seed_x = master(), seed_y = master() and the strings are
+ * generate_random(m, alphabet, seed_x) / generate_random(n, alphabet, seed_y)
+ * (io.cpp:103-115).  Same procedure as wlcs_generate_pairs
+ * (include/wavelcs_capi.h); tests/test_oracle.py checks they agree byte for
+ * byte.  xs / ys must hold pairs * hi bytes, offsets pairs + 1 entries. */
+void orc_generate_pairs(size_t pairs, size_t lo, size_t hi, const uint8_t* alphabet, size_t alen,
+                        uint64_t seed, uint8_t* xs, uint64_t* x_off, uint8_t* ys,
+                        uint64_t* y_off) {
+    mt64_t master;
+    mt64_seed(&master, seed);
+    uint64_t xo = 0, yo = 0;
+    x_off[0] = y_off[0] = 0;
+    for (size_t k = 0; k < pairs; ++k) {
+        const size_t m = lo + (size_t)(mt64_next(&master) % (uint64_t)(hi - lo + 1));
+        const size_t n = lo + (size_t)(mt64_next(&master) % (uint64_t)(hi - lo + 1));
+        const uint64_t sx = mt64_next(&master), sy = mt64_next(&master);
+        orc_generate_random(m, alphabet, alen, sx, xs + xo);
+        orc_generate_random(n, alphabet, alen, sy, ys + yo);
+        xo += m;
+        yo += n;
+        x_off[k + 1] = xo;
+        y_off[k + 1] = yo;
+    }
+}

@@ -122,6 +122,7 @@ lib.wlcs_ipc_handle.argtypes = [_vp, ctypes.c_char_p]
 lib.wlcs_ipc_open.argtypes = [ctypes.c_char_p, ctypes.POINTER(ctypes.c_void_p)]
 lib.wlcs_ipc_close.argtypes = [_vp]
 lib.wlcs_fill_tables.argtypes = [_vp, _sz, _vp, _sz, _sz, _vp, _vp]
+lib.wlcs_colsplit_emulate.argtypes = [_vp, _sz, _vp, _sz, ctypes.c_int, ctypes.c_int, _u32p]
 lib.wlcs_length_batch_multi.argtypes = [_vp, _u64p, _vp, _u64p, _sz, ctypes.c_int,
                                         ctypes.POINTER(ctypes.c_uint32)]
 lib.wlcs_length_strips.argtypes = [_vp, _sz, _vp, _sz, ctypes.c_int,
@@ -301,6 +302,17 @@ def lcs_length_strips(x, y, n_gpus: int) -> int:
     xb, yb = _as_bytes(x), _as_bytes(y)
     out = ctypes.c_uint32()
     _check(lib.wlcs_length_strips(xb, len(xb), yb, len(yb), n_gpus, ctypes.byref(out)))
+    return int(out.value)
+
+
+def colsplit_emulate(x, y, slices: int, max_ctas: int = 0) -> int:
+    """The multi-GPU column split of (x rows, y columns) with `slices` ranks
+    played as CTA pools of ONE launch on the current device (the inboxes are
+    filled and polled while both sides run).  max_ctas caps the grid."""
+    xb, yb = _as_bytes(x), _as_bytes(y)
+    out = ctypes.c_uint32()
+    _check(lib.wlcs_colsplit_emulate(xb, len(xb), yb, len(yb), slices, max_ctas,
+                                     ctypes.byref(out)))
     return int(out.value)
 
 

@@ -120,9 +120,13 @@ __global__ void __launch_bounds__(kPlanThreads) batch_plan_kernel(BatchDev d, ui
             const uint64_t w = (cols + 31) / 32;
             const uint64_t kmax = uint64_t(d.kmax);
             if (w > 32 * kmax || rows > (uint64_t(1) << 30)) {
-                // Wider than one warp can hold: routed to the single-pair strip kernel.
-                const uint32_t i = atomicAdd(d.meta + kMetaOverflow, 1u);
-                d.overflow[i] = p;
+                // Wider than one warp's lane shapes: the second pass (bitpar_wide.cu)
+                // sweeps it in column blocks -- or, when the host holds the
+                // offsets, the single-pair strip kernel (long_to_host).
+                if (!(d.long_to_host && w > 32 * kmax)) {
+                    const uint32_t i = atomicAdd(d.meta + kMetaOverflow, 1u);
+                    d.overflow[i] = p;
+                }
             } else {
                 int sidx = 0;
                 while ((kmax << sidx) < w) ++sidx;
@@ -138,9 +142,20 @@ __global__ void __launch_bounds__(kPlanThreads) batch_plan_kernel(BatchDev d, ui
         }
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < kBuckets; i += blockDim.x) {
-        const uint32_t c = local[i];
-        if (c) local[i] = atomicAdd(hist + i, c);  // block base inside bucket i
+    {
+        // block base inside every bucket: the kBuckets / kPlanThreads returning
+        // atomics of a thread are issued back to back (all in flight at once)
+        constexpr int kPer = kBuckets / kPlanThreads;
+        static_assert(kBuckets % kPlanThreads == 0, "bucket split");
+        uint32_t c[kPer], base[kPer];
+#pragma unroll
+        for (int k = 0; k < kPer; ++k) c[k] = local[threadIdx.x + k * kPlanThreads];
+#pragma unroll
+        for (int k = 0; k < kPer; ++k)
+            base[k] = c[k] ? atomicAdd(hist + threadIdx.x + k * kPlanThreads, c[k]) : 0u;
+#pragma unroll
+        for (int k = 0; k < kPer; ++k)
+            if (c[k]) local[threadIdx.x + k * kPlanThreads] = base[k];
     }
     __syncthreads();
     if (i < d.pairs) {
@@ -338,49 +353,6 @@ __device__ __forceinline__ TaskInfo decode_task(const TaskTable& tt, uint32_t t)
 // every code's match mask is the AND over the planes of "plane == bit of the
 // code's byte value": a handful of LOP3 per (code, word), written once --
 // no read-modify-write, no dependency chains, ALU only.
-__device__ __forceinline__ uint64_t transpose8x8(uint64_t x) {
-    uint64_t t = (x ^ (x >> 7)) & 0x00AA00AA00AA00AAull;
-    x = x ^ t ^ (t << 7);
-    t = (x ^ (x >> 14)) & 0x0000CCCC0000CCCCull;
-    x = x ^ t ^ (t << 14);
-    t = (x ^ (x >> 28)) & 0x00000000F0F0F0F0ull;
-    return x ^ t ^ (t << 28);
-}
-
-// 32 column bytes (8 words, byte j of the word = column j) -> 8 bit-planes.
-__device__ __forceinline__ void bit_planes(const uint32_t* w, uint32_t* P) {
-    uint32_t lo[4], hi[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        const uint64_t y = transpose8x8(uint64_t(w[2 * q]) | (uint64_t(w[2 * q + 1]) << 32));
-        lo[q] = uint32_t(y);          // planes 0..3, 8 columns each
-        hi[q] = uint32_t(y >> 32);    // planes 4..7
-    }
-#pragma unroll
-    for (int b = 0; b < 4; ++b) {
-        const uint32_t sel = 0x0040u | uint32_t(b) | (uint32_t(b) << 4);  // bytes b of x, y
-        P[b] = __byte_perm(__byte_perm(lo[0], lo[1], sel), __byte_perm(lo[2], lo[3], sel), 0x5410);
-        P[b + 4] =
-            __byte_perm(__byte_perm(hi[0], hi[1], sel), __byte_perm(hi[2], hi[3], sel), 0x5410);
-    }
-}
-
-// The 32 column bytes of the lane's word k, realigned out of the 16-byte
-// aligned chunks 2k, 2k+1, 2k+2 (q = a_c / 4, fs = 8 * (a_c % 4)).
-__device__ __forceinline__ void word_bytes(const uint4& c0, const uint4& c1, const uint4& c2, int q,
-                                           uint32_t fs, uint32_t* w) {
-    const uint32_t W[12] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w, c2.x, c2.y, c2.z, c2.w};
-    uint32_t lo[9];
-#pragma unroll
-    for (int i = 0; i < 9; ++i) {
-        const uint32_t a = (q & 1) ? W[i + 1] : W[i];
-        const uint32_t b2 = (q & 1) ? W[i + 3] : W[i + 2];
-        lo[i] = (q & 2) ? b2 : a;
-    }
-#pragma unroll
-    for (int i = 0; i < 8; ++i) w[i] = __funnelshift_r(lo[i], lo[i + 1], fs);
-}
-
 // Builds the task's byte -> code map and match masks in shared memory.  K is
 // a runtime value and every loop over words / codes is rolled: the build is
 // one small piece of code shared by all lane shapes (it runs once per task
@@ -537,8 +509,8 @@ __device__ __forceinline__ uint32_t build_task(const BatchDev& d, const LanePair
             uint32_t w0[8], w1[8], P0[8], P1[8];
             word_bytes(c0v, c1v, c2v, q, fs, w0);
             word_bytes(c2v, c3v, c4v, q, fs, w1);
-            bit_planes(w0, P0);
-            bit_planes(w1, P1);
+            bit_planes8(w0, P0);
+            bit_planes8(w1, P1);
             const bool has1 = k + 1 < K;  // warp-uniform
             const int nv0 = min(max(clen - 32 * k, 0), 32);
             const int nv1 = has1 ? min(max(clen - 32 * (k + 1), 0), 32) : 0;
@@ -591,7 +563,7 @@ __device__ __forceinline__ uint32_t build_task(const BatchDev& d, const LanePair
             const uint4 n1 = chunk2(2 * k + 3), n2 = chunk2(2 * k + 4);
             uint32_t w[8], P[8];
             word_bytes(c0v, c1v, c2v, q, fs, w);
-            bit_planes(w, P);
+            bit_planes8(w, P);
             const int nv = min(max(clen - 32 * k, 0), 32);
             const uint32_t vmask = nv >= 32 ? 0xffffffffu : ((1u << nv) - 1u);
             const uint32_t woff =

@@ -114,18 +114,8 @@ struct StoreHook {
     }
 };
 
-__device__ __forceinline__ uint32_t ld_relaxed_gpu(const uint32_t* p) {
-    uint32_t v;
-    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-// System-scope variants for the carry words that cross GPUs (column split:
+// System-scope variant for the carry words that cross GPUs (column split:
 // the producer writes into the consumer's memory over NVLink / P2P).
-__device__ __forceinline__ uint32_t ld_relaxed_sys(const uint32_t* p) {
-    uint32_t v;
-    asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
 __device__ __forceinline__ uint4 ld_relaxed_sys_v4(const uint32_t* p) {
     uint4 v;
     asm volatile("ld.relaxed.sys.global.v4.u32 {%0, %1, %2, %3}, [%4];"
@@ -134,14 +124,12 @@ __device__ __forceinline__ uint4 ld_relaxed_sys_v4(const uint32_t* p) {
                  : "memory");
     return v;
 }
-// L2-only (cache-global) vector load for polling self-validating words: a
-// weak load that always goes to L2, re-issued because the asm is volatile;
-// no ordering against the thread's own earlier stores is required here.
-__device__ __forceinline__ uint4 ld_cg_v4(const uint32_t* p) {
+__device__ __forceinline__ uint4 ld_relaxed_gpu_v4(const uint32_t* p) {
     uint4 v;
-    asm volatile("ld.global.cg.v4.u32 {%0, %1, %2, %3}, [%4];"
+    asm volatile("ld.relaxed.gpu.global.v4.u32 {%0, %1, %2, %3}, [%4];"
                  : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-                 : "l"(p));
+                 : "l"(p)
+                 : "memory");
     return v;
 }
 
@@ -159,6 +147,10 @@ __device__ __forceinline__ void st_relaxed_sys_nb(uint32_t* p, uint32_t v) {
 }
 
 constexpr uint32_t kCarryValid = 0x10000u;  // carry words: valid flag | 16-row mask
+// re-polls of one carry group before a strip gives up (about 10-30 s of L2 /
+// NVLink round trips: far beyond any legitimate wait, which is bounded by the
+// producer's own fill time)
+constexpr uint32_t kPollLimit = 1u << 24;
 
 // Row coding: entry i = map[row byte i] (the row's match-mask record in the
 // strip's shared-memory table is at code * code_stride).  Rows
@@ -192,9 +184,11 @@ __global__ void pair_code_rows_kernel(const uint8_t* row, int64_t rows, int reve
     }
 }
 
-// Strip kernel.  Tickets t = 0, 1, ... map to (problem t % nprob, strip
-// t / nprob), so inside each problem strips start in order and a strip only
-// ever waits on a strip that is already running.
+// Strip kernel.  CTA b serves problem q = b % nprob and takes its strips
+// from ticket[q] in increasing order, so inside each problem strips start in
+// order and a strip only ever waits on a strip that is already running (or, in
+// a column split, on the neighbouring slice's last strip, served by another
+// pool).
 //
 // Per step a lane reads its 16-row chunk as 16 codes (4 coalesced LDG.128,
 // prefetched kCodeAhead steps ahead) and runs 16 row updates: per row one
@@ -204,12 +198,13 @@ __global__ void pair_code_rows_kernel(const uint8_t* row, int64_t rows, int reve
 // Carry handoff between strips: lane 31 of strip s publishes the 16-row carry
 // mask of chunk ch as one relaxed 32-bit store (kCarryValid | mask) into a
 // zero-initialised buffer -- the data word is its own ready flag, so no fence
-// is needed.  Strip s+1 reads the words four chunks at a time (one 16-byte
-// relaxed load, the same address for the whole warp: a broadcast, so the
-// hand-off code is warp-uniform), two groups of four steps ahead; a group
-// with a word still 0 when loaded is re-polled.  Inside the warp the carry masks move with two
-// shuffles per step (rows 0-7 after row 7, rows 8-15 after row 15), so the
-// shuffle latency hides behind row work.
+// is needed.  Strip s+1 reads the words four chunks at a time with one 16-byte
+// relaxed load (gpu scope; sys scope for a neighbour GPU's inbox), the same
+// address for the whole warp: a broadcast, so the hand-off code is
+// warp-uniform.  The load of group g+1 is issued when group g is consumed; a
+// group with a word still 0 is re-polled.  Inside the warp the carry masks
+// move with two shuffles per step (rows 0-7 after row 7, rows 8-15 after row
+// 15), so the shuffle latency hides behind row work.
 //
 // Launch: 1-warp CTAs (one strip each), up to the occupancy limit (more
 // warps per CTA were measured: no gain, strips only share sub-partitions).
@@ -221,13 +216,14 @@ __global__ void __launch_bounds__(32, 1) pair_strip_kernel(PairDev d) {
     const uint32_t lane = lane_id();
     const uint32_t lane_off = PmLayout<K>::word_offset(lane, 0);
     uint32_t* sink = d.sink + (int64_t(blockIdx.x) * blockDim.x + threadIdx.x);
+    const int q = int(blockIdx.x % uint32_t(d.nprob));
+    const FillProblem& P = d.prob[q];
     for (;;) {
         uint32_t tk = 0;
-        if (lane == 0) tk = atomicAdd(d.ticket, 1u);
+        if (lane == 0) tk = atomicAdd(d.ticket + q, 1u);
         tk = __shfl_sync(kFullMask, tk, 0);
-        if (tk >= uint32_t(d.nprob * d.prob[0].nstrips)) break;
-        const FillProblem& P = d.prob[tk % uint32_t(d.nprob)];
-        const uint32_t strip = tk / uint32_t(d.nprob);
+        if (tk >= uint32_t(P.nstrips)) break;
+        const uint32_t strip = tk;
         __syncwarp();
         const int64_t g = int64_t(strip) * 32 + lane;  // global lane-group index
         for (int c = 0; c < d.sigma; ++c) {
@@ -258,11 +254,8 @@ __global__ void __launch_bounds__(32, 1) pair_strip_kernel(PairDev d) {
         // the whole warp loads the (same) carry words -- a broadcast, so the
         // hand-off code is warp-uniform (no divergence); lane 0 consumes them
         const bool feeder = has_left;
-        auto carry_ld = [&](const uint32_t* q) {
-            return ext_left ? ld_relaxed_sys(q) : ld_relaxed_gpu(q);
-        };
-        auto carry_ld4 = [&](const uint32_t* q) {
-            return ext_left ? ld_relaxed_sys_v4(q) : ld_cg_v4(q);
+        auto carry_ld4 = [&](const uint32_t* p) {
+            return ext_left ? ld_relaxed_sys_v4(p) : ld_relaxed_gpu_v4(p);
         };
         StoreHook<K, STORE> hook{
             STORE ? P.rows_out + ((int64_t(strip) * P.Dpad) * 32 + lane) * K : nullptr, 0};
@@ -270,9 +263,7 @@ __global__ void __launch_bounds__(32, 1) pair_strip_kernel(PairDev d) {
         // lane l works on chunk t - l (chunks < 0 / >= nchunks are padding).
         // Register rings, no rotation moves (a move of a register with a load
         // in flight would stall on it): codes of step t live in ring slot
-        // t % 4 and are reloaded, 4 steps ahead, right after their rows; the
-        // left strip's carry words (4 chunks per 16-byte relaxed load) are
-        // loaded one group of 4 steps ahead.
+        // t % 4 and are reloaded, 4 steps ahead, right after their rows.
         // Lane 0's chunk is always new data (an L2 round trip), the other
         // lanes re-read what lane l-1 read a step earlier.
         const int64_t cstride = P.cstride;
@@ -284,23 +275,12 @@ __global__ void __launch_bounds__(32, 1) pair_strip_kernel(PairDev d) {
 #pragma unroll
         for (int j = 0; j < kCodeAhead; ++j) ring[j] = load_codes(cp + j * cstride);
         cp += kCodeAhead * cstride;
-        // carry words travel global -> shared memory by cp.async two groups of
-        // 4 steps ahead (no register waits on a load in flight); ring of 4
-        // 16-byte slots per warp after the match masks
+        // the left strip's carry words: group g+1 (chunks 4g+4 .. 4g+7) is
+        // loaded when group g is consumed -- a whole group of steps ahead, so
+        // the load has landed when its value is moved (carry rows are padded
+        // by 16 words past the last chunk)
         uint4 cw = make_uint4(0, 0, 0, 0);
-        uint4* cring = reinterpret_cast<uint4*>(smem + d.pm_warp_bytes);
-        const uint32_t cring_s = uint32_t(__cvta_generic_to_shared(cring));
-        auto carry_async = [&](int g) {  // group g's words -> slot g % 4 (lane 0)
-            if (lane == 0)
-                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
-                                 cring_s + uint32_t(g & 3) * 16u),
-                             "l"(left_carry + 4 * g));
-            asm volatile("cp.async.commit_group;");
-        };
-        if (feeder) {
-            carry_async(0);
-            if (d.carry_ahead > 1) carry_async(1);
-        }
+        uint4 cw_next = feeder ? carry_ld4(left_carry) : make_uint4(0, 0, 0, 0);
         const uint8_t* pml = pm + lane_off;
         const uint32_t csr = d.code_stride;  // runtime value: address IMAD stays on the FMA pipe
         // carry-in masks of the current step, rows 0-7 / 8-15 at bits 31..24
@@ -309,17 +289,20 @@ __global__ void __launch_bounds__(32, 1) pair_strip_kernel(PairDev d) {
         uint32_t cin_lo = 0, cin_hi = 0;
         for (int tg = 0; tg < T; tg += 4) {
             if (feeder && tg < nchunks) {
-                if (d.carry_ahead > 1) asm volatile("cp.async.wait_group 1;" ::: "memory");
-                else asm volatile("cp.async.wait_group 0;" ::: "memory");  // group tg/4 landed
-                __syncwarp();
-                cw = cring[(tg >> 2) & 3];
+                cw = cw_next;
                 const int lim = nchunks - tg;  // words at or past nchunks stay 0
+                uint32_t spins = 0;
                 while ((cw.x == 0u) | (lim > 1 && cw.y == 0u) | (lim > 2 && cw.z == 0u) |
                        (lim > 3 && cw.w == 0u)) {
                     cw = carry_ld4(left_carry + tg);  // not yet published: re-poll
+                    if (++spins > kPollLimit) {
+                        // watchdog: a producer that never publishes (a dead peer
+                        // GPU, a broken inbox) fails the call instead of hanging it
+                        if (lane == 0) atomicOr(d.error, 1u);
+                        return;
+                    }
                 }
-                __syncwarp();
-                carry_async((tg >> 2) + d.carry_ahead);
+                cw_next = carry_ld4(left_carry + tg + 4);
                 prefetch_l2(left_carry + tg + 16);
             }
 #pragma unroll
@@ -371,7 +354,6 @@ __global__ void __launch_bounds__(32, 1) pair_strip_kernel(PairDev d) {
                 cin_hi = nh << 24;
             }
         }
-        if (feeder) asm volatile("cp.async.wait_all;" ::: "memory");  // ring reused next strip
         __syncwarp();
         if (P.v_out) {
 #pragma unroll
@@ -968,7 +950,6 @@ static cudaError_t launch_strip(const PairDev& dev, int sms, cudaStream_t stream
     PairDev d = dev;
     d.code_stride = uint32_t(pair_code_stride(K));
     d.pm_warp_bytes = uint32_t(d.sigma * pair_code_stride(K));
-    d.carry_ahead = 1;  // carry-word groups staged ahead (2 measured slower)
     const int smem = pair_smem_bytes(K, d.sigma);
     cudaError_t e = cudaFuncSetAttribute(pair_strip_kernel<K, STORE>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -977,10 +958,13 @@ static cudaError_t launch_strip(const PairDev& dev, int sms, cudaStream_t stream
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pair_strip_kernel<K, STORE>, 32, smem);
     if (e != cudaSuccess) return e;
     if (occ < 1) occ = 1;
-    const int strips = d.nprob * d.prob[0].nstrips;
+    int strips = 0;
+    for (int q = 0; q < d.nprob; ++q) strips += d.prob[q].nstrips;
     int grid = strips;
     if (grid > sms * occ) grid = sms * occ;
+    if (d.max_ctas > 0 && grid > d.max_ctas) grid = d.max_ctas;
     if (grid * 32 > kPairSinkWords) grid = kPairSinkWords / 32;
+    if (grid < d.nprob) grid = d.nprob;  // every problem needs a pool of at least one warp
     pair_strip_kernel<K, STORE><<<grid, 32, smem, stream>>>(d);
     return cudaGetLastError();
 }

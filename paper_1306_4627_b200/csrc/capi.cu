@@ -81,6 +81,7 @@ struct Ctx {
     bool timing = false;          // wlcs_set_timing: bracket the main kernel with events
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     float last_main_ms = -1.f;
+    bool timing_pending = false;  // ev0/ev1 recorded by an asynchronous call, not yet read
     int sms = 148;
     cudaStream_t stream = nullptr;
     cudaStream_t copy_stream = nullptr;  // host batch pipeline: H2D of chunk k+1 || compute of k
@@ -89,13 +90,15 @@ struct Ctx {
     // call: a pageable destination would make each one a staged, synchronous
     // copy (~10 us) inside the caller's timed region
     uint64_t* hscratch = nullptr;
-    // batch
-    DevBuf xs, ys, xoff, yoff, out, ws, ws2;
+    cudaEvent_t join_ev = nullptr;       // orders c.stream after a caller's stream
+    // batch (ws: first pass per chunk; ws2 + wcarry: the device second pass)
+    DevBuf xs, ys, xoff, yoff, out, ws, ws2, wcarry;
     // single pair
     DevBuf px, py, pmg, carry, small, rows, outrev, codes, ry, vbuf, wave, sink, walk;
     ~Ctx() {
         if (hscratch) cudaFreeHost(hscratch);
         for (cudaEvent_t e : chunk_ev) cudaEventDestroy(e);
+        if (join_ev) cudaEventDestroy(join_ev);
         if (copy_stream) cudaStreamDestroy(copy_stream);
         if (stream) cudaStreamDestroy(stream);
     }
@@ -159,6 +162,23 @@ cudaError_t stream_wait(cudaStream_t s) {
         if (std::chrono::steady_clock::now() - t0 > std::chrono::microseconds(3000))
             return cudaStreamSynchronize(s);
     }
+}
+
+// A NULL stream from the caller means the legacy default stream (torch's
+// default stream, plain <<<>>> launches): never the library's own stream,
+// which is non-blocking and therefore unordered with it.
+cudaStream_t caller_stream(void* stream) {
+    return stream ? static_cast<cudaStream_t>(stream) : cudaStreamLegacy;
+}
+
+// Orders the library's per-thread stream after the work the caller enqueued
+// on `user` before this call (an event, no host wait).
+int join_caller(Ctx& c, cudaStream_t user) {
+    if (user == c.stream) return WLCS_OK;
+    if (!c.join_ev) WLCS_CUDA(cudaEventCreateWithFlags(&c.join_ev, cudaEventDisableTiming));
+    WLCS_CUDA(cudaEventRecord(c.join_ev, user));
+    WLCS_CUDA(cudaStreamWaitEvent(c.stream, c.join_ev, 0));
+    return WLCS_OK;
 }
 
 int env_int(const char* name, int dflt) {
@@ -255,8 +275,25 @@ bool use_split(int64_t rows, bool store) {
 // Prepares alphabet, match masks and buffers for the pair (row, col).  With
 // `split` the rows are cut in half and the bottom half runs on the reversed
 // strings as a second problem of the same launch (length only).
-// small: present[256] u32 @0 | map[256] u16 @1024 | sigma @1536 | ticket @1540 |
-//        zeros u64 @1544 | walk len u64 @1552 | safe16 @2048
+// small: present[256] u32 @0 | map[256] u16 @1024 | sigma @1536 |
+//        zeros u64 @1544 | walk len u64 @1552 | walk misses u32[3] @1560 |
+//        strip tickets u32[kMaxProblems] @1664 | safe16 @2048
+constexpr int kTicketOff = 1664;
+constexpr int kErrOff = 1596;  // strip-kernel watchdog flag (zeroed with the tickets)
+
+// Enqueues the read of the strip kernel's watchdog flag into hscratch[7];
+// after the stream wait, watchdog_failed() tells whether a carry poll timed out.
+int watchdog_read(Ctx& c, cudaStream_t s) {
+    WLCS_CUDA(cudaMemcpyAsync(c.hscratch + 7, c.small.as<uint8_t>() + kErrOff, 4,
+                              cudaMemcpyDeviceToHost, s));
+    return WLCS_OK;
+}
+int watchdog_failed(Ctx& c) {
+    if (uint32_t(c.hscratch[7]) == 0) return WLCS_OK;
+    return fail(WLCS_E_INTERNAL,
+                "strip kernel: carry words of a neighbouring slice never arrived (watchdog)");
+}
+
 int pair_setup(Ctx& c, const uint8_t* d_row, int64_t rows, const uint8_t* d_col, int64_t cols,
                bool store, PairPlan& plan) {
     wlcs::PairDev& d = plan.d;
@@ -269,7 +306,8 @@ int pair_setup(Ctx& c, const uint8_t* d_row, int64_t rows, const uint8_t* d_col,
     uint32_t* present = reinterpret_cast<uint32_t*>(sb);
     uint16_t* map = reinterpret_cast<uint16_t*>(sb + 1024);
     uint32_t* sigma_dev = reinterpret_cast<uint32_t*>(sb + 1536);
-    d.ticket = reinterpret_cast<uint32_t*>(sb + 1540);
+    d.ticket = reinterpret_cast<uint32_t*>(sb + kTicketOff);
+    d.error = reinterpret_cast<uint32_t*>(sb + kErrOff);
     WLCS_CUDA(c.sink.ensure(size_t(wlcs::kPairSinkWords) * 4));
     d.sink = c.sink.as<uint32_t>();
     unsigned long long* zeros = reinterpret_cast<unsigned long long*>(sb + 1544);
@@ -317,7 +355,7 @@ int pair_setup(Ctx& c, const uint8_t* d_row, int64_t rows, const uint8_t* d_col,
         carry += size_t(d.prob[q].nstrips) * size_t(d.prob[q].cwords);
     }
     WLCS_CUDA(cudaMemsetAsync(c.carry.p, 0, carry_words * 4, c.stream));
-    WLCS_CUDA(cudaMemsetAsync(d.ticket, 0, 4 + 4 + 8 + 8, c.stream));
+    WLCS_CUDA(cudaMemsetAsync(sb + 1540, 0, kTicketOff + 4 * wlcs::kMaxProblems - 1540, c.stream));
     WLCS_CUDA(cudaMemsetAsync(sb + 2048, 0, 16, c.stream));
     if (store) {
         const size_t bytes =
@@ -364,8 +402,13 @@ int pair_length_device(Ctx& c, const uint8_t* dx, size_t m, const uint8_t* dy, s
                                            zeros, c.stream));
     }
     WLCS_CUDA(cudaMemcpyAsync(c.hscratch, zeros, 8, cudaMemcpyDeviceToHost, c.stream));
+    if (int rc2 = watchdog_read(c, c.stream)) return rc2;
     WLCS_CUDA(stream_wait(c.stream));
-    if (c.timing) WLCS_CUDA(cudaEventElapsedTime(&c.last_main_ms, c.ev0, c.ev1));
+    if (int rc2 = watchdog_failed(c)) return rc2;
+    if (c.timing) {
+        WLCS_CUDA(cudaEventElapsedTime(&c.last_main_ms, c.ev0, c.ev1));
+        c.timing_pending = false;
+    }
     *out = uint32_t(c.hscratch[0]);
     return WLCS_OK;
 }
@@ -410,7 +453,10 @@ int pair_wave_device(Ctx& c, const uint8_t* dx, size_t m, const uint8_t* dy, siz
     if (c.timing) WLCS_CUDA(cudaEventRecord(c.ev1, c.stream));
     WLCS_CUDA(cudaMemcpyAsync(out, d.out, 4, cudaMemcpyDeviceToHost, c.stream));
     WLCS_CUDA(stream_wait(c.stream));
-    if (c.timing) WLCS_CUDA(cudaEventElapsedTime(&c.last_main_ms, c.ev0, c.ev1));
+    if (c.timing) {
+        WLCS_CUDA(cudaEventElapsedTime(&c.last_main_ms, c.ev0, c.ev1));
+        c.timing_pending = false;
+    }
     return WLCS_OK;
 }
 
@@ -421,84 +467,24 @@ int pair_length_variant(Ctx& c, const uint8_t* dx, size_t m, const uint8_t* dy, 
 }
 
 // ------------------------------------------------------------------ batch
-// Second batch pass over the pairs the first pass could not take because
-// their column alphabet did not fit the warp's mask budget: one word per lane
-// (128-byte code rows, so every byte alphabet fits in 257 * 128 bytes).
-// `d` describes the first pass (its offsets / outputs); `list` is its device
-// overflow list of n entries.  Pairs still left (wider than 32 words, or all
-// 256 byte values present) are returned in `left` for the strip kernel.
-int batch_overflow_pass(Ctx& c, wlcs::BatchDev d, const uint32_t* list, uint32_t n,
-                        cudaStream_t s, std::vector<uint32_t>& left) {
-    left.clear();
-    if (n == 0) return WLCS_OK;
-    d.ids = list;
-    d.pairs = n;
-    d.kmax = 1;
-    d.pm_bytes = 257 * 128;
-    WLCS_CUDA(c.ws2.ensure(wlcs::batch_workspace_bytes(n, d.pm_bytes)));
-    WLCS_CUDA(wlcs::batch_launch(d, c.ws2.p, c.sms, s));
-    uint32_t* h2 = reinterpret_cast<uint32_t*>(c.hscratch + 1);
-    WLCS_CUDA(cudaMemcpyAsync(h2, wlcs::batch_overflow_count_ptr(c.ws2.p, n), 4,
-                              cudaMemcpyDeviceToHost, s));
-    WLCS_CUDA(stream_wait(s));
-    const uint32_t n2 = *h2;
-    if (n2 == 0) return WLCS_OK;
-    left.resize(n2);
-    WLCS_CUDA(cudaMemcpy(left.data(), wlcs::batch_overflow_list_ptr(c.ws2.p, n), n2 * 4,
-                         cudaMemcpyDeviceToHost));
-    return WLCS_OK;
+// Words of the shorter string above which a pair leaves the first pass's lane
+// shapes (bitpar_batch.cu: w > 32 * kmax).
+bool batch_is_long(uint64_t m, uint64_t n, int kmax) {
+    const uint64_t cols = m < n ? m : n;
+    return (cols + 31) / 32 > uint64_t(32) * uint64_t(kmax);
 }
 
-int batch_device(Ctx& c, const uint8_t* d_xs, const uint64_t* d_xoff, const uint8_t* d_ys,
-                 const uint64_t* d_yoff, size_t pairs, uint64_t xs_bytes, uint64_t ys_bytes,
-                 int variant, uint32_t* d_out, cudaStream_t stream) {
+// Enqueues one batch on `s` (device pointers, nothing waits on the host):
+// the first pass (plan, scatter, main) and the second pass over the first
+// pass's overflow list (bitpar_wide.cu; the list length is read on the
+// device, so an empty second pass is two short launches).  With
+// `long_to_host` the pairs too wide for the first pass are skipped -- the
+// host entry points run them through the strip kernel instead.
+int batch_enqueue(Ctx& c, const uint8_t* d_xs, const uint64_t* d_xoff, const uint8_t* d_ys,
+                  const uint64_t* d_yoff, size_t pairs, uint64_t xs_bytes, uint64_t ys_bytes,
+                  uint32_t* d_out, cudaStream_t s, void* ws, bool long_to_host, bool ev_start,
+                  bool ev_end) {
     if (pairs == 0) return WLCS_OK;
-    if (pairs > 0x7fffffffull) return fail(WLCS_E_INVALID_ARGUMENT, "too many pairs in one batch");
-    if (variant != WLCS_VARIANT_BITPARALLEL && variant != WLCS_VARIANT_WAVEFRONT)
-        return fail(WLCS_E_CONFIG, "unknown fill variant " + std::to_string(variant));
-    if (variant == WLCS_VARIANT_WAVEFRONT) {
-        WLCS_CUDA(c.ws.ensure(8 + size_t(pairs) * 4));
-        wlcs::WaveBatchDev d{};
-        d.xs = d_xs;
-        d.xoff = d_xoff;
-        d.ys = d_ys;
-        d.yoff = d_yoff;
-        d.out = d_out;
-        d.pairs = uint32_t(pairs);
-        d.counter = c.ws.as<uint32_t>();
-        d.overflow_count = d.counter + 1;
-        d.overflow = d.counter + 2;
-        WLCS_CUDA(cudaMemsetAsync(d.counter, 0, 8, stream));
-        if (c.timing && !c.ev0) {
-            WLCS_CUDA(cudaEventCreate(&c.ev0));
-            WLCS_CUDA(cudaEventCreate(&c.ev1));
-        }
-        if (c.timing) WLCS_CUDA(cudaEventRecord(c.ev0, stream));
-        WLCS_CUDA(wlcs::wave_batch_launch(d, c.sms, stream));
-        if (c.timing) WLCS_CUDA(cudaEventRecord(c.ev1, stream));
-        uint32_t* hov = reinterpret_cast<uint32_t*>(c.hscratch);
-        WLCS_CUDA(cudaMemcpyAsync(hov, d.overflow_count, 4, cudaMemcpyDeviceToHost, stream));
-        WLCS_CUDA(stream_wait(stream));
-        const uint32_t overflow = *hov;
-        if (c.timing) WLCS_CUDA(cudaEventElapsedTime(&c.last_main_ms, c.ev0, c.ev1));
-        if (overflow == 0) return WLCS_OK;
-        std::vector<uint32_t> ids(overflow);
-        WLCS_CUDA(cudaMemcpy(ids.data(), d.overflow, overflow * 4, cudaMemcpyDeviceToHost));
-        for (uint32_t p : ids) {
-            uint64_t xo[2], yo[2];
-            WLCS_CUDA(cudaMemcpy(xo, d_xoff + p, 16, cudaMemcpyDeviceToHost));
-            WLCS_CUDA(cudaMemcpy(yo, d_yoff + p, 16, cudaMemcpyDeviceToHost));
-            uint32_t len = 0;
-            int rc = pair_wave_device(c, d_xs + xo[0], size_t(xo[1] - xo[0]), d_ys + yo[0],
-                                      size_t(yo[1] - yo[0]), &len);
-            if (rc) return rc;
-            WLCS_CUDA(cudaMemcpy(d_out + p, &len, 4, cudaMemcpyHostToDevice));
-        }
-        return WLCS_OK;
-    }
-    const int pm_bytes = batch_pm_bytes();
-    const size_t ws_bytes = wlcs::batch_workspace_bytes(uint32_t(pairs), pm_bytes);
-    WLCS_CUDA(c.ws.ensure(ws_bytes));
     wlcs::BatchDev d{};
     d.xs = d_xs;
     d.xoff = d_xoff;
@@ -508,53 +494,97 @@ int batch_device(Ctx& c, const uint8_t* d_xs, const uint64_t* d_xoff, const uint
     d.ys_bytes = ys_bytes;
     d.out = d_out;
     d.pairs = uint32_t(pairs);
-    d.pm_bytes = pm_bytes;
-        d.kmax = batch_kmax();
+    d.pm_bytes = batch_pm_bytes();
+    d.kmax = batch_kmax();
+    d.long_to_host = long_to_host ? 1 : 0;
+    if ((ev_start || ev_end) && !c.ev0) {
+        WLCS_CUDA(cudaEventCreate(&c.ev0));
+        WLCS_CUDA(cudaEventCreate(&c.ev1));
+    }
+    WLCS_CUDA(wlcs::batch_launch(d, ws, c.sms, s, ev_start ? c.ev0 : nullptr,
+                                 ev_end ? c.ev1 : nullptr));
+    if (ev_end) c.timing_pending = true;
+    const size_t words = wlcs::wide_scratch_words(xs_bytes, ys_bytes, uint32_t(pairs));
+    WLCS_CUDA(c.ws2.ensure(wlcs::wide_workspace_bytes(uint32_t(pairs))));
+    WLCS_CUDA(c.wcarry.ensure(2 * words * sizeof(uint16_t)));
+    wlcs::WideDev w{};
+    w.xs = d_xs;
+    w.xoff = d_xoff;
+    w.xs_bytes = xs_bytes;
+    w.ys = d_ys;
+    w.yoff = d_yoff;
+    w.ys_bytes = ys_bytes;
+    w.out = d_out;
+    w.list = wlcs::batch_overflow_list_ptr(ws, uint32_t(pairs));
+    w.count = wlcs::batch_overflow_count_ptr(ws, uint32_t(pairs));
+    w.cap = uint32_t(pairs);
+    w.pairs_total = uint32_t(pairs);
+    w.carry[0] = c.wcarry.as<uint16_t>();
+    w.carry[1] = c.wcarry.as<uint16_t>() + words;
+    WLCS_CUDA(wlcs::wide_launch(w, c.ws2.p, c.sms, s));
+    return WLCS_OK;
+}
+
+// Cell-wavefront variant of the batch (wavefront.cu): one kernel; pairs whose
+// shorter string exceeds its shared-memory row go through the single-pair
+// wavefront kernel afterwards (ids and offsets read back once, lengths
+// written into d_out on the caller's stream).
+int batch_wave(Ctx& c, const uint8_t* d_xs, const uint64_t* d_xoff, const uint8_t* d_ys,
+               const uint64_t* d_yoff, size_t pairs, uint32_t* d_out, cudaStream_t stream) {
+    WLCS_CUDA(c.ws.ensure(8 + size_t(pairs) * 4));
+    wlcs::WaveBatchDev d{};
+    d.xs = d_xs;
+    d.xoff = d_xoff;
+    d.ys = d_ys;
+    d.yoff = d_yoff;
+    d.out = d_out;
+    d.pairs = uint32_t(pairs);
+    d.counter = c.ws.as<uint32_t>();
+    d.overflow_count = d.counter + 1;
+    d.overflow = d.counter + 2;
+    WLCS_CUDA(cudaMemsetAsync(d.counter, 0, 8, stream));
     if (c.timing && !c.ev0) {
         WLCS_CUDA(cudaEventCreate(&c.ev0));
         WLCS_CUDA(cudaEventCreate(&c.ev1));
     }
-    WLCS_CUDA(wlcs::batch_launch(d, c.ws.p, c.sms, stream, c.timing ? c.ev0 : nullptr,
-                                 c.timing ? c.ev1 : nullptr));
+    if (c.timing) WLCS_CUDA(cudaEventRecord(c.ev0, stream));
+    WLCS_CUDA(wlcs::wave_batch_launch(d, c.sms, stream));
+    if (c.timing) {
+        WLCS_CUDA(cudaEventRecord(c.ev1, stream));
+        c.timing_pending = true;
+    }
     uint32_t* hov = reinterpret_cast<uint32_t*>(c.hscratch);
-    WLCS_CUDA(cudaMemcpyAsync(hov, wlcs::batch_overflow_count_ptr(c.ws.p, uint32_t(pairs)),
-                              4, cudaMemcpyDeviceToHost, stream));
+    WLCS_CUDA(cudaMemcpyAsync(hov, d.overflow_count, 4, cudaMemcpyDeviceToHost, stream));
     WLCS_CUDA(stream_wait(stream));
     const uint32_t overflow = *hov;
-    if (c.timing) WLCS_CUDA(cudaEventElapsedTime(&c.last_main_ms, c.ev0, c.ev1));
-    if (overflow && env_int("WLCS_DEBUG_BATCH", 0)) {
-        std::vector<uint32_t> ids(overflow);
-        WLCS_CUDA(cudaMemcpy(ids.data(), wlcs::batch_overflow_list_ptr(c.ws.p, uint32_t(pairs)),
-                             overflow * 4, cudaMemcpyDeviceToHost));
-        std::fprintf(stderr, "wlcs batch: %u pairs to the second pass:", overflow);
-        for (uint32_t i = 0; i < overflow && i < 16; ++i) std::fprintf(stderr, " %u", ids[i]);
-        std::fprintf(stderr, "\n");
-    }
     if (overflow == 0) return WLCS_OK;
-    // Alphabet too large for the lane shape: second pass at one word per lane;
-    // pairs too long for one warp: strip kernel.
-    std::vector<uint32_t> ids;
-    if (int rc = batch_overflow_pass(c, d, wlcs::batch_overflow_list_ptr(c.ws.p, uint32_t(pairs)),
-                                     overflow, stream, ids))
-        return rc;
-    for (uint32_t p : ids) {
-        uint64_t xo[2], yo[2];
-        WLCS_CUDA(cudaMemcpy(xo, d_xoff + p, 16, cudaMemcpyDeviceToHost));
-        WLCS_CUDA(cudaMemcpy(yo, d_yoff + p, 16, cudaMemcpyDeviceToHost));
-        uint32_t len = 0;
-        int rc = pair_length_device(c, d_xs + xo[0], size_t(xo[1] - xo[0]), d_ys + yo[0],
-                                    size_t(yo[1] - yo[0]), &len);
-        if (rc) return rc;
-        WLCS_CUDA(cudaMemcpy(d_out + p, &len, 4, cudaMemcpyHostToDevice));
+    std::vector<uint32_t> ids(overflow);
+    WLCS_CUDA(cudaMemcpyAsync(ids.data(), d.overflow, overflow * 4, cudaMemcpyDeviceToHost, stream));
+    WLCS_CUDA(stream_wait(stream));
+    std::vector<uint64_t> xo(2 * size_t(overflow)), yo(2 * size_t(overflow));
+    for (uint32_t k = 0; k < overflow; ++k) {
+        WLCS_CUDA(cudaMemcpyAsync(&xo[2 * k], d_xoff + ids[k], 16, cudaMemcpyDeviceToHost, stream));
+        WLCS_CUDA(cudaMemcpyAsync(&yo[2 * k], d_yoff + ids[k], 16, cudaMemcpyDeviceToHost, stream));
     }
+    WLCS_CUDA(stream_wait(stream));
+    std::vector<uint32_t> lens(overflow);
+    for (uint32_t k = 0; k < overflow; ++k) {
+        int rc = pair_wave_device(c, d_xs + xo[2 * k], size_t(xo[2 * k + 1] - xo[2 * k]),
+                                  d_ys + yo[2 * k], size_t(yo[2 * k + 1] - yo[2 * k]), &lens[k]);
+        if (rc) return rc;
+    }
+    for (uint32_t k = 0; k < overflow; ++k)
+        WLCS_CUDA(cudaMemcpyAsync(d_out + ids[k], &lens[k], 4, cudaMemcpyHostToDevice, stream));
+    WLCS_CUDA(stream_wait(stream));  // lens is a local array
     return WLCS_OK;
 }
 
 // Host batch with the host->device copies pipelined against the compute:
 // the pairs are cut into nchunks contiguous chunks; chunk k's string bytes are
 // copied on copy_stream while chunk k-1 runs on the compute stream (its own
-// workspace, so the chunks' plans never overlap).  Overflow pairs (too long
-// or too large an alphabet for one warp) are finished afterwards.
+// first-pass workspace, so the chunks' plans never overlap; the second pass's
+// workspace is reused in stream order).  Pairs wider than the first pass's
+// lane shapes are finished afterwards by the strip kernel (batch_long_pairs).
 int batch_host_pipelined(Ctx& c, const uint8_t* xs, const uint64_t* x_off, const uint8_t* ys,
                          const uint64_t* y_off, size_t pairs, int nchunks, uint32_t* out) {
     const uint64_t xs_bytes = x_off[pairs], ys_bytes = y_off[pairs];
@@ -577,10 +607,6 @@ int batch_host_pipelined(Ctx& c, const uint8_t* xs, const uint64_t* x_off, const
     uint8_t* dys = c.ys.as<uint8_t>();
     WLCS_CUDA(cudaMemcpyAsync(c.xoff.p, x_off, (pairs + 1) * 8, cudaMemcpyHostToDevice, cs));
     WLCS_CUDA(cudaMemcpyAsync(c.yoff.p, y_off, (pairs + 1) * 8, cudaMemcpyHostToDevice, cs));
-    if (c.timing && !c.ev0) {
-        WLCS_CUDA(cudaEventCreate(&c.ev0));
-        WLCS_CUDA(cudaEventCreate(&c.ev1));
-    }
     for (int k = 0; k < nchunks; ++k) {
         const uint64_t xa = x_off[p0[k]], xb = x_off[p0[k + 1]];
         const uint64_t ya = y_off[p0[k]], yb = y_off[p0[k + 1]];
@@ -588,64 +614,28 @@ int batch_host_pipelined(Ctx& c, const uint8_t* xs, const uint64_t* x_off, const
         if (yb > ya) WLCS_CUDA(cudaMemcpyAsync(dys + ya, ys + ya, yb - ya, cudaMemcpyHostToDevice, cs));
         WLCS_CUDA(cudaEventRecord(c.chunk_ev[k], cs));
         WLCS_CUDA(cudaStreamWaitEvent(s, c.chunk_ev[k], 0));
-        wlcs::BatchDev d{};
-        d.xs = dxs;
-        d.xoff = c.xoff.as<uint64_t>() + p0[k];
-        d.xs_bytes = xs_bytes;
-        d.ys = dys;
-        d.yoff = c.yoff.as<uint64_t>() + p0[k];
-        d.ys_bytes = ys_bytes;
-        d.out = c.out.as<uint32_t>() + p0[k];
-        d.pairs = uint32_t(p0[k + 1] - p0[k]);
-        d.pm_bytes = pm_bytes;
-        d.kmax = batch_kmax();
-        const bool ends = k == 0 || k == nchunks - 1;
-        WLCS_CUDA(wlcs::batch_launch(d, c.ws.as<uint8_t>() + ws_off[k], c.sms, s,
-                                     (c.timing && ends && k == 0) ? c.ev0 : nullptr,
-                                     (c.timing && ends && k == nchunks - 1) ? c.ev1 : nullptr));
+        if (int rc = batch_enqueue(c, dxs, c.xoff.as<uint64_t>() + p0[k], dys,
+                                   c.yoff.as<uint64_t>() + p0[k], p0[k + 1] - p0[k], xs_bytes,
+                                   ys_bytes, c.out.as<uint32_t>() + p0[k], s,
+                                   c.ws.as<uint8_t>() + ws_off[k], true,
+                                   c.timing && k == 0, c.timing && k == nchunks - 1))
+            return rc;
     }
     WLCS_CUDA(cudaMemcpyAsync(out, c.out.p, pairs * 4, cudaMemcpyDeviceToHost, s));
-    // per-chunk overflow counts into the pinned scratch (<= 64 chunks)
-    uint32_t* ovf = reinterpret_cast<uint32_t*>(c.hscratch);
-    for (int k = 0; k < nchunks; ++k)
-        WLCS_CUDA(cudaMemcpyAsync(&ovf[k],
-                                  wlcs::batch_overflow_count_ptr(c.ws.as<uint8_t>() + ws_off[k],
-                                                                 uint32_t(p0[k + 1] - p0[k])),
-                                  4, cudaMemcpyDeviceToHost, s));
     WLCS_CUDA(stream_wait(s));
-    const std::vector<uint32_t> ovf_n(ovf, ovf + nchunks);  // the scratch is reused below
-    if (c.timing) WLCS_CUDA(cudaEventElapsedTime(&c.last_main_ms, c.ev0, c.ev1));
-    std::vector<std::vector<uint32_t>> left(nchunks);
-    bool second = false;
-    for (int k = 0; k < nchunks; ++k) {
-        if (!ovf_n[k]) continue;
-        wlcs::BatchDev d{};
-        d.xs = dxs;
-        d.xoff = c.xoff.as<uint64_t>() + p0[k];
-        d.xs_bytes = xs_bytes;
-        d.ys = dys;
-        d.yoff = c.yoff.as<uint64_t>() + p0[k];
-        d.ys_bytes = ys_bytes;
-        d.out = c.out.as<uint32_t>() + p0[k];
-        if (int rc = batch_overflow_pass(
-                c, d,
-                wlcs::batch_overflow_list_ptr(c.ws.as<uint8_t>() + ws_off[k],
-                                              uint32_t(p0[k + 1] - p0[k])),
-                ovf_n[k], s, left[k]))
-            return rc;
-        second = true;
-    }
-    if (second)
-        WLCS_CUDA(cudaMemcpy(out, c.out.p, pairs * 4, cudaMemcpyDeviceToHost));
-    for (int k = 0; k < nchunks; ++k) {
-        for (uint32_t q : left[k]) {
-            const size_t p = p0[k] + q;
-            uint32_t len = 0;
-            int rc = pair_length_device(c, dxs + x_off[p], size_t(x_off[p + 1] - x_off[p]),
-                                        dys + y_off[p], size_t(y_off[p + 1] - y_off[p]), &len);
-            if (rc) return rc;
-            out[p] = len;
-        }
+    return WLCS_OK;
+}
+
+// Pairs the first pass cannot hold (batch_is_long) through the single-pair
+// strip kernel, straight from the device copy of the strings.
+int batch_long_pairs(Ctx& c, const uint8_t* dxs, const uint8_t* dys, const uint64_t* x_off,
+                     const uint64_t* y_off, const std::vector<size_t>& ids, uint32_t* out) {
+    for (size_t p : ids) {
+        uint32_t len = 0;
+        int rc = pair_length_device(c, dxs + x_off[p], size_t(x_off[p + 1] - x_off[p]),
+                                    dys + y_off[p], size_t(y_off[p + 1] - y_off[p]), &len);
+        if (rc) return rc;
+        out[p] = len;
     }
     return WLCS_OK;
 }
@@ -658,6 +648,181 @@ int validate_offsets(const uint64_t* off, size_t pairs, const char* name) {
     return WLCS_OK;
 }
 
+
+// ---- column split of G slices inside ONE launch on one device ------------
+// The multi-GPU column split (wlcs_colsplit_fill per rank) with every rank's
+// slice played as its own pair of problems (forward + reverse) of a single
+// strip-kernel launch: slice g's first strips poll inboxes that slice g-1 /
+// g+1's last strips fill while running -- the same fused hand-off as between
+// GPUs, but the "ranks" are co-resident CTA pools of one grid (no separate
+// launches that wait on each other).  max_ctas caps the grid so that a test
+// can run with fewer warps per pool than strips per problem (liveness).
+// L = max_k F[k] + R[N-k] as in wlcs_length_strips.
+int split_combine_host(int G, const std::vector<size_t>& lo, const std::vector<size_t>& hi,
+                       const std::vector<std::vector<uint32_t>>& vf,
+                       const std::vector<std::vector<uint32_t>>& vr, size_t N, uint32_t* out) {
+    std::vector<int64_t> F(N + 1, 0), R(N + 1, 0);
+    size_t k = 0;
+    for (int g = 0; g < G; ++g)
+        for (size_t c = 0; c < hi[g] - lo[g]; ++c, ++k)
+            F[k + 1] = F[k] + (((vf[g][c >> 5] >> (c & 31)) & 1u) ? 0 : 1);
+    k = 0;
+    for (int g = G - 1; g >= 0; --g)
+        for (size_t c = 0; c < hi[g] - lo[g]; ++c, ++k)
+            R[k + 1] = R[k] + (((vr[g][c >> 5] >> (c & 31)) & 1u) ? 0 : 1);
+    int64_t best = 0;
+    for (size_t kk = 0; kk <= N; ++kk) best = std::max(best, F[kk] + R[N - kk]);
+    *out = uint32_t(best);
+    return WLCS_OK;
+}
+
+}  // namespace
+
+extern "C" int wlcs_colsplit_emulate(const uint8_t* x, size_t m, const uint8_t* y, size_t n,
+                                     int slices, int max_ctas, uint32_t* out) {
+    if (!x || !y || !out) return fail(WLCS_E_INVALID_ARGUMENT, "NULL argument");
+    const int G = slices;
+    if (G < 1 || 2 * G > wlcs::kMaxProblems)
+        return fail(WLCS_E_INVALID_ARGUMENT, "slices must be 1 .. " +
+                                                 std::to_string(wlcs::kMaxProblems / 2));
+    if (m < 2 || n < size_t(32) * size_t(G))
+        return fail(WLCS_E_INVALID_ARGUMENT, "column split needs m >= 2 and n >= 32 * slices");
+    Ctx* c = nullptr;
+    int rc = get_ctx(&c);
+    if (rc) return rc;
+    WLCS_CUDA(c->px.ensure(m + 16));
+    WLCS_CUDA(c->py.ensure(n + 16));
+    WLCS_CUDA(c->ry.ensure(n + 16));
+    WLCS_CUDA(cudaMemcpyAsync(c->px.p, x, m, cudaMemcpyHostToDevice, c->stream));
+    WLCS_CUDA(cudaMemcpyAsync(c->py.p, y, n, cudaMemcpyHostToDevice, c->stream));
+    const uint8_t* dx = c->px.as<uint8_t>();
+    const uint8_t* dy = c->py.as<uint8_t>();
+    uint8_t* dry = c->ry.as<uint8_t>();
+    WLCS_CUDA(wlcs::pair_reverse(dy, int64_t(n), dry, c->stream));
+    // slice bounds on word boundaries (wlcs_length_strips)
+    std::vector<size_t> lo(G), hi(G);
+    const size_t words = (n + 31) / 32;
+    for (int g = 0; g < G; ++g) {
+        lo[g] = std::min(n, words * g / G * 32);
+        hi[g] = std::min(n, words * (g + 1) / G * 32);
+    }
+    wlcs::PairDev d{};
+    d.colp0 = dy;
+    d.prob[0].cols = int64_t(n);  // alphabet of the whole column string
+    WLCS_CUDA(c->small.ensure(4096));
+    uint8_t* sb = c->small.as<uint8_t>();
+    uint16_t* map = reinterpret_cast<uint16_t*>(sb + 1024);
+    d.ticket = reinterpret_cast<uint32_t*>(sb + kTicketOff);
+    d.error = reinterpret_cast<uint32_t*>(sb + kErrOff);
+    d.safe16 = reinterpret_cast<const uint4*>(sb + 2048);
+    WLCS_CUDA(c->sink.ensure(size_t(wlcs::kPairSinkWords) * 4));
+    d.sink = c->sink.as<uint32_t>();
+    int sigma = 0;
+    WLCS_CUDA(wlcs::pair_prepare(d, reinterpret_cast<uint32_t*>(sb), map,
+                                 reinterpret_cast<uint32_t*>(sb + 1536), c->stream, &sigma));
+    const int64_t mid = int64_t(m / 2);
+    int64_t wmax = 0;
+    for (int g = 0; g < G; ++g) wmax = std::max<int64_t>(wmax, int64_t(hi[g] - lo[g] + 31) / 32);
+    const int K = choose_k(*c, wmax, int64_t(m) - mid, sigma, 2 * G);
+    if (wlcs::pair_smem_bytes(K, sigma) > 220 * 1024)
+        return fail(WLCS_E_INTERNAL, "match-mask table does not fit in shared memory");
+    d.nprob = 2 * G;
+    d.max_ctas = max_ctas;
+    // per problem: masks [sigma][W_g]; final vectors; carries
+    size_t pm_total = 0, v_total = 0;
+    for (int g = 0; g < G; ++g) {
+        const size_t Wg = (hi[g] - lo[g] + 31) / 32;
+        pm_total += 2 * size_t(sigma) * Wg;
+        v_total += 2 * Wg;
+    }
+    WLCS_CUDA(c->pmg.ensure(pm_total * 4));
+    WLCS_CUDA(c->vbuf.ensure(v_total * 4 + 64));
+    // row codes are shared by every slice of a direction
+    wlcs::FillProblem fwd{}, rev{};
+    fwd.rows = mid;
+    fwd.nchunks = int((mid + 15) / 16);
+    rev.rows = int64_t(m) - mid;
+    rev.nchunks = int((rev.rows + 15) / 16);
+    const size_t code_vecs =
+        4 * size_t(wlcs::pair_code_plane(fwd.nchunks) + wlcs::pair_code_plane(rev.nchunks));
+    WLCS_CUDA(c->codes.ensure(code_vecs * 16));
+    uint4* code_base = c->codes.as<uint4>();
+    WLCS_CUDA(wlcs::pair_code_rows(dx, fwd.rows, false, map, K, fwd, code_base, c->stream));
+    WLCS_CUDA(wlcs::pair_code_rows(dx + mid, rev.rows, true, map, K, rev,
+                                   code_base + 4 * wlcs::pair_code_plane(fwd.nchunks), c->stream));
+    size_t inbox_words = 0;
+    rc = wlcs_colsplit_inbox_words(m, &inbox_words);
+    if (rc) return rc;
+    size_t carry_words = 2 * size_t(G) * inbox_words;  // inboxes first
+    uint32_t* pmg = c->pmg.as<uint32_t>();
+    uint32_t* vb = c->vbuf.as<uint32_t>();
+    for (int g = 0; g < G; ++g) {
+        const int64_t cols = int64_t(hi[g] - lo[g]);
+        const int64_t Wg = (cols + 31) / 32;
+        for (int dir = 0; dir < 2; ++dir) {
+            wlcs::FillProblem& P = d.prob[2 * g + dir];
+            const wlcs::FillProblem& R = dir == 0 ? fwd : rev;
+            set_problem(P, R.rows, pmg, cols, K);
+            P.coded = R.coded;
+            P.plane = R.plane;
+            P.cstride = R.cstride;
+            P.v_out = vb;
+            WLCS_CUDA(wlcs::pair_build_pm(dir == 0 ? dy + lo[g] : dry + (n - hi[g]), cols, map,
+                                          sigma, Wg, pmg, c->stream));
+            pmg += size_t(sigma) * size_t(Wg);
+            vb += Wg;
+            carry_words += size_t(P.nstrips) * size_t(P.cwords);
+        }
+    }
+    WLCS_CUDA(c->carry.ensure(carry_words * 4 + 256));
+    uint32_t* inbox_f = c->carry.as<uint32_t>();                         // [G][inbox_words]
+    uint32_t* inbox_r = inbox_f + size_t(G) * inbox_words;               // [G][inbox_words]
+    uint32_t* carry = inbox_r + size_t(G) * inbox_words;
+    for (int g = 0; g < G; ++g) {
+        wlcs::FillProblem& F = d.prob[2 * g];
+        wlcs::FillProblem& R = d.prob[2 * g + 1];
+        F.ext_in = g > 0 ? inbox_f + size_t(g) * inbox_words : nullptr;
+        F.ext_out = g + 1 < G ? inbox_f + size_t(g + 1) * inbox_words : nullptr;
+        R.ext_in = g + 1 < G ? inbox_r + size_t(g) * inbox_words : nullptr;
+        R.ext_out = g > 0 ? inbox_r + size_t(g - 1) * inbox_words : nullptr;
+        for (wlcs::FillProblem* P : {&F, &R}) {
+            P->carry = carry;
+            carry += size_t(P->nstrips) * size_t(P->cwords);
+        }
+    }
+    WLCS_CUDA(cudaMemsetAsync(c->carry.p, 0, carry_words * 4, c->stream));
+    WLCS_CUDA(cudaMemsetAsync(sb + 1540, 0, kTicketOff + 4 * wlcs::kMaxProblems - 1540, c->stream));
+    WLCS_CUDA(cudaMemsetAsync(sb + 2048, 0, 16, c->stream));
+    if (c->timing && !c->ev0) {
+        WLCS_CUDA(cudaEventCreate(&c->ev0));
+        WLCS_CUDA(cudaEventCreate(&c->ev1));
+    }
+    if (c->timing) WLCS_CUDA(cudaEventRecord(c->ev0, c->stream));
+    WLCS_CUDA(wlcs::pair_fill(d, K, false, c->sms, c->stream));
+    if (c->timing) WLCS_CUDA(cudaEventRecord(c->ev1, c->stream));
+    std::vector<uint32_t> vall(v_total);
+    WLCS_CUDA(cudaMemcpyAsync(vall.data(), c->vbuf.p, v_total * 4, cudaMemcpyDeviceToHost, c->stream));
+    rc = watchdog_read(*c, c->stream);
+    if (rc) return rc;
+    WLCS_CUDA(stream_wait(c->stream));
+    rc = watchdog_failed(*c);
+    if (rc) return rc;
+    if (c->timing) {
+        WLCS_CUDA(cudaEventElapsedTime(&c->last_main_ms, c->ev0, c->ev1));
+        c->timing_pending = false;
+    }
+    std::vector<std::vector<uint32_t>> vf(G), vr(G);
+    size_t off = 0;
+    for (int g = 0; g < G; ++g) {
+        const size_t Wg = (hi[g] - lo[g] + 31) / 32;
+        vf[g].assign(vall.begin() + off, vall.begin() + off + Wg);
+        vr[g].assign(vall.begin() + off + Wg, vall.begin() + off + 2 * Wg);
+        off += 2 * Wg;
+    }
+    return split_combine_host(G, lo, hi, vf, vr, n, out);
+}
+
+namespace {
 }  // namespace
 
 extern "C" {
@@ -710,7 +875,6 @@ int wlcs_length(const uint8_t* x, size_t m, const uint8_t* y, size_t n, size_t m
 
 int wlcs_length_device(const uint8_t* d_x, size_t m, const uint8_t* d_y, size_t n, int variant,
                        uint32_t* out, void* stream) {
-    (void)stream;
     if (!out) return fail(WLCS_E_INVALID_ARGUMENT, "out is NULL");
     if ((reinterpret_cast<uintptr_t>(d_x) | reinterpret_cast<uintptr_t>(d_y)) & 15u)
         return fail(WLCS_E_INVALID_ARGUMENT, "device string buffers must be 16-byte aligned");
@@ -719,6 +883,9 @@ int wlcs_length_device(const uint8_t* d_x, size_t m, const uint8_t* d_y, size_t 
     if (rc) return rc;
     if (variant != WLCS_VARIANT_BITPARALLEL && variant != WLCS_VARIANT_WAVEFRONT)
         return fail(WLCS_E_CONFIG, "unknown fill variant " + std::to_string(variant));
+    // the strings may still be in flight on the caller's stream
+    rc = join_caller(*c, caller_stream(stream));
+    if (rc) return rc;
     return pair_length_variant(*c, d_x, m, d_y, n, variant, out);
 }
 
@@ -762,7 +929,10 @@ int wlcs_subsequence(const uint8_t* x, size_t m, const uint8_t* y, size_t n,
     WLCS_CUDA(cudaMemcpyAsync(c->hscratch + 1, zeros_dev, 8, cudaMemcpyDeviceToHost, c->stream));
     WLCS_CUDA(stream_wait(c->stream));
     const unsigned long long len = c->hscratch[0], zeros = c->hscratch[1];
-    if (c->timing) WLCS_CUDA(cudaEventElapsedTime(&c->last_main_ms, c->ev0, c->ev1));
+    if (c->timing) {
+        WLCS_CUDA(cudaEventElapsedTime(&c->last_main_ms, c->ev0, c->ev1));
+        c->timing_pending = false;
+    }
     if (env_int("WLCS_DEBUG_WALK", 0)) {
         uint32_t miss[3] = {0, 0, 0};
         WLCS_CUDA(cudaMemcpy(miss, dmiss, 12, cudaMemcpyDeviceToHost));
@@ -787,18 +957,31 @@ int wlcs_length_batch_device(const uint8_t* d_xs, const uint64_t* d_x_off, const
                              uint64_t ys_bytes, int variant, uint32_t* d_out, void* stream) {
     if ((reinterpret_cast<uintptr_t>(d_xs) | reinterpret_cast<uintptr_t>(d_ys)) & 15u)
         return fail(WLCS_E_INVALID_ARGUMENT, "device string buffers must be 16-byte aligned");
+    if (pairs > 0x7fffffffull) return fail(WLCS_E_INVALID_ARGUMENT, "too many pairs in one batch");
+    if (variant != WLCS_VARIANT_BITPARALLEL && variant != WLCS_VARIANT_WAVEFRONT)
+        return fail(WLCS_E_CONFIG, "unknown fill variant " + std::to_string(variant));
     Ctx* c = nullptr;
     int rc = get_ctx(&c);
     if (rc) return rc;
-    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : c->stream;
-    return batch_device(*c, d_xs, d_x_off, d_ys, d_y_off, pairs, xs_bytes, ys_bytes, variant,
-                        d_out, s);
+    if (pairs == 0) return WLCS_OK;
+    const cudaStream_t s = caller_stream(stream);
+    if (variant == WLCS_VARIANT_WAVEFRONT) {
+        rc = join_caller(*c, s);
+        if (rc) return rc;
+        return batch_wave(*c, d_xs, d_x_off, d_ys, d_y_off, pairs, d_out, s);
+    }
+    WLCS_CUDA(c->ws.ensure(wlcs::batch_workspace_bytes(uint32_t(pairs), batch_pm_bytes())));
+    return batch_enqueue(*c, d_xs, d_x_off, d_ys, d_y_off, pairs, xs_bytes, ys_bytes, d_out, s,
+                         c->ws.p, false, c->timing, c->timing);
 }
 
 int wlcs_length_batch_ex(const uint8_t* xs, const uint64_t* x_off, const uint8_t* ys,
                          const uint64_t* y_off, size_t pairs, int variant, uint32_t* out) {
     if (pairs == 0) return WLCS_OK;
     if (!x_off || !y_off || !out) return fail(WLCS_E_INVALID_ARGUMENT, "NULL argument");
+    if (pairs > 0x7fffffffull) return fail(WLCS_E_INVALID_ARGUMENT, "too many pairs in one batch");
+    if (variant != WLCS_VARIANT_BITPARALLEL && variant != WLCS_VARIANT_WAVEFRONT)
+        return fail(WLCS_E_CONFIG, "unknown fill variant " + std::to_string(variant));
     int rc = validate_offsets(x_off, pairs, "x");
     if (rc) return rc;
     rc = validate_offsets(y_off, pairs, "y");
@@ -814,23 +997,43 @@ int wlcs_length_batch_ex(const uint8_t* xs, const uint64_t* x_off, const uint8_t
     WLCS_CUDA(c->yoff.ensure((pairs + 1) * 8));
     WLCS_CUDA(c->out.ensure(pairs * 4));
     cudaStream_t s = c->stream;
+    // pairs too wide for the first pass's lane shapes: strip kernel (the
+    // host knows the offsets, so they never reach the device second pass)
+    std::vector<size_t> long_ids;
+    if (variant == WLCS_VARIANT_BITPARALLEL) {
+        const int kmax = batch_kmax();
+        for (size_t k = 0; k < pairs; ++k)
+            if (batch_is_long(x_off[k + 1] - x_off[k], y_off[k + 1] - y_off[k], kmax))
+                long_ids.push_back(k);
+    }
     const int nchunks = variant == WLCS_VARIANT_BITPARALLEL
                             ? int(std::min<size_t>(std::min<size_t>(size_t(env_int("WLCS_BATCH_CHUNKS", 4)), 64),
                                                    pairs / 8192))
                             : 1;
-    if (nchunks >= 2 && xs_bytes + ys_bytes >= (16u << 20))
-        return batch_host_pipelined(*c, xs, x_off, ys, y_off, pairs, nchunks, out);
+    if (nchunks >= 2 && xs_bytes + ys_bytes >= (16u << 20)) {
+        rc = batch_host_pipelined(*c, xs, x_off, ys, y_off, pairs, nchunks, out);
+        if (rc) return rc;
+        return batch_long_pairs(*c, c->xs.as<uint8_t>(), c->ys.as<uint8_t>(), x_off, y_off,
+                                long_ids, out);
+    }
     if (xs_bytes) WLCS_CUDA(cudaMemcpyAsync(c->xs.p, xs, xs_bytes, cudaMemcpyHostToDevice, s));
     if (ys_bytes) WLCS_CUDA(cudaMemcpyAsync(c->ys.p, ys, ys_bytes, cudaMemcpyHostToDevice, s));
     WLCS_CUDA(cudaMemcpyAsync(c->xoff.p, x_off, (pairs + 1) * 8, cudaMemcpyHostToDevice, s));
     WLCS_CUDA(cudaMemcpyAsync(c->yoff.p, y_off, (pairs + 1) * 8, cudaMemcpyHostToDevice, s));
-    rc = batch_device(*c, c->xs.as<uint8_t>(), c->xoff.as<uint64_t>(), c->ys.as<uint8_t>(),
-                      c->yoff.as<uint64_t>(), pairs, xs_bytes, ys_bytes, variant,
-                      c->out.as<uint32_t>(), s);
+    if (variant == WLCS_VARIANT_WAVEFRONT) {
+        rc = batch_wave(*c, c->xs.as<uint8_t>(), c->xoff.as<uint64_t>(), c->ys.as<uint8_t>(),
+                        c->yoff.as<uint64_t>(), pairs, c->out.as<uint32_t>(), s);
+    } else {
+        WLCS_CUDA(c->ws.ensure(wlcs::batch_workspace_bytes(uint32_t(pairs), batch_pm_bytes())));
+        rc = batch_enqueue(*c, c->xs.as<uint8_t>(), c->xoff.as<uint64_t>(), c->ys.as<uint8_t>(),
+                           c->yoff.as<uint64_t>(), pairs, xs_bytes, ys_bytes,
+                           c->out.as<uint32_t>(), s, c->ws.p, true, c->timing, c->timing);
+    }
     if (rc) return rc;
     WLCS_CUDA(cudaMemcpyAsync(out, c->out.p, pairs * 4, cudaMemcpyDeviceToHost, s));
     WLCS_CUDA(stream_wait(s));
-    return WLCS_OK;
+    return batch_long_pairs(*c, c->xs.as<uint8_t>(), c->ys.as<uint8_t>(), x_off, y_off, long_ids,
+                            out);
 }
 
 int wlcs_length_batch(const uint8_t* xs, const uint64_t* x_off, const uint8_t* ys,
@@ -844,6 +1047,7 @@ int wlcs_set_timing(int on) {
     if (rc) return rc;
     c->timing = on != 0;
     c->last_main_ms = -1.f;
+    c->timing_pending = false;
     return WLCS_OK;
 }
 
@@ -851,6 +1055,11 @@ int wlcs_last_kernel_ms(float* ms) {
     Ctx* c = nullptr;
     int rc = get_ctx(&c);
     if (rc) return rc;
+    if (c->timing_pending) {  // an asynchronous batch: wait for its end event only
+        WLCS_CUDA(cudaEventSynchronize(c->ev1));
+        WLCS_CUDA(cudaEventElapsedTime(&c->last_main_ms, c->ev0, c->ev1));
+        c->timing_pending = false;
+    }
     *ms = c->last_main_ms;
     return WLCS_OK;
 }
@@ -946,7 +1155,8 @@ int wlcs_colsplit_fill(const uint8_t* x, size_t m, const uint8_t* y, size_t n, s
     WLCS_CUDA(c->small.ensure(4096));
     uint8_t* sb = c->small.as<uint8_t>();
     uint16_t* map = reinterpret_cast<uint16_t*>(sb + 1024);
-    d.ticket = reinterpret_cast<uint32_t*>(sb + 1540);
+    d.ticket = reinterpret_cast<uint32_t*>(sb + kTicketOff);
+    d.error = reinterpret_cast<uint32_t*>(sb + kErrOff);
     d.safe16 = reinterpret_cast<const uint4*>(sb + 2048);
     WLCS_CUDA(c->sink.ensure(size_t(wlcs::kPairSinkWords) * 4));
     d.sink = c->sink.as<uint32_t>();
@@ -996,7 +1206,8 @@ int wlcs_colsplit_fill(const uint8_t* x, size_t m, const uint8_t* y, size_t n, s
         carry += size_t(d.prob[k].nstrips) * size_t(d.prob[k].cwords);
     }
     WLCS_CUDA(cudaMemsetAsync(c->carry.p, 0, carry_words * 4, c->stream));
-    WLCS_CUDA(cudaMemsetAsync(d.ticket, 0, 4, c->stream));
+    WLCS_CUDA(cudaMemsetAsync(d.ticket, 0, 4 * wlcs::kMaxProblems, c->stream));
+    WLCS_CUDA(cudaMemsetAsync(d.error, 0, 4, c->stream));
     WLCS_CUDA(cudaMemsetAsync(sb + 2048, 0, 16, c->stream));
     if (want[0]) WLCS_CUDA(wlcs::pair_build_pm(dcol, cols, map, sigma, W, pmg, c->stream));
     if (want[1]) {
@@ -1018,8 +1229,15 @@ int wlcs_colsplit_fill(const uint8_t* x, size_t m, const uint8_t* y, size_t n, s
     if (want[1] && v_rev)
         WLCS_CUDA(cudaMemcpyAsync(v_rev, c->vbuf.as<uint32_t>() + W, size_t(W) * 4,
                                   cudaMemcpyDeviceToHost, c->stream));
+    rc = watchdog_read(*c, c->stream);
+    if (rc) return rc;
     WLCS_CUDA(stream_wait(c->stream));
-    if (c->timing) WLCS_CUDA(cudaEventElapsedTime(&c->last_main_ms, c->ev0, c->ev1));
+    rc = watchdog_failed(*c);
+    if (rc) return rc;
+    if (c->timing) {
+        WLCS_CUDA(cudaEventElapsedTime(&c->last_main_ms, c->ev0, c->ev1));
+        c->timing_pending = false;
+    }
     return WLCS_OK;
 }
 
@@ -1191,20 +1409,8 @@ int wlcs_length_strips(const uint8_t* x, size_t m, const uint8_t* y, size_t n, i
     cleanup();
     for (int g = 0; g < G; ++g)
         if (rcs[g]) return fail(rcs[g], "device " + std::to_string(g) + ": " + errs[g]);
-    // combine: L = max_k F[k] + R[k] (multigpu.py: colsplit_combine)
-    std::vector<int64_t> F(N + 1, 0), R(N + 1, 0);
-    size_t k = 0;
-    for (int g = 0; g < G; ++g)
-        for (size_t c = 0; c < hi[g] - lo[g]; ++c, ++k)
-            F[k + 1] = F[k] + (((vf[g][c >> 5] >> (c & 31)) & 1u) ? 0 : 1);
-    k = 0;
-    for (int g = G - 1; g >= 0; --g)
-        for (size_t c = 0; c < hi[g] - lo[g]; ++c, ++k)
-            R[k + 1] = R[k] + (((vr[g][c >> 5] >> (c & 31)) & 1u) ? 0 : 1);
-    int64_t best = 0;
-    for (size_t kk = 0; kk <= N; ++kk) best = std::max(best, F[kk] + R[N - kk]);
-    *out = uint32_t(best);
-    return WLCS_OK;
+    // combine: L = max_k F[k] + R[N-k] (multigpu.py: colsplit_combine)
+    return split_combine_host(G, lo, hi, vf, vr, N, out);
 }
 
 // ------------------------------------------------------- full tables

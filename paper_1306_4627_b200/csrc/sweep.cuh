@@ -321,4 +321,54 @@ __device__ __forceinline__ int lane_zero_count(const uint32_t* V, int64_t word0,
     return zeros;
 }
 
+// ---------------------------------------------------------------------------
+// Match-mask build helpers (batch kernels): 32 column bytes -> 8 bit-planes.
+// Each lane owns 32-column words of its pair's column string; per word it
+// (1) realigns the 32 column bytes out of 16-byte aligned chunks (funnel
+// shifts), (2) turns them into 8 bit-planes with four 8x8 bit transposes
+// (plane b, bit j = bit b of column j's byte).  A code's match mask is then
+// the AND over the planes of "plane == bit of the code's byte value".
+__device__ __forceinline__ uint64_t transpose8x8(uint64_t x) {
+    uint64_t t = (x ^ (x >> 7)) & 0x00AA00AA00AA00AAull;
+    x = x ^ t ^ (t << 7);
+    t = (x ^ (x >> 14)) & 0x0000CCCC0000CCCCull;
+    x = x ^ t ^ (t << 14);
+    t = (x ^ (x >> 28)) & 0x00000000F0F0F0F0ull;
+    return x ^ t ^ (t << 28);
+}
+
+// 32 column bytes (8 words, byte j of the word = column j) -> 8 bit-planes.
+__device__ __forceinline__ void bit_planes8(const uint32_t* w, uint32_t* P) {
+    uint32_t lo[4], hi[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const uint64_t y = transpose8x8(uint64_t(w[2 * q]) | (uint64_t(w[2 * q + 1]) << 32));
+        lo[q] = uint32_t(y);          // planes 0..3, 8 columns each
+        hi[q] = uint32_t(y >> 32);    // planes 4..7
+    }
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+        const uint32_t sel = 0x0040u | uint32_t(b) | (uint32_t(b) << 4);  // bytes b of x, y
+        P[b] = __byte_perm(__byte_perm(lo[0], lo[1], sel), __byte_perm(lo[2], lo[3], sel), 0x5410);
+        P[b + 4] =
+            __byte_perm(__byte_perm(hi[0], hi[1], sel), __byte_perm(hi[2], hi[3], sel), 0x5410);
+    }
+}
+
+// The 32 column bytes of the lane's word k, realigned out of the 16-byte
+// aligned chunks 2k, 2k+1, 2k+2 (q = a_c / 4, fs = 8 * (a_c % 4)).
+__device__ __forceinline__ void word_bytes(const uint4& c0, const uint4& c1, const uint4& c2, int q,
+                                           uint32_t fs, uint32_t* w) {
+    const uint32_t W[12] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w, c2.x, c2.y, c2.z, c2.w};
+    uint32_t lo[9];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) {
+        const uint32_t a = (q & 1) ? W[i + 1] : W[i];
+        const uint32_t b2 = (q & 1) ? W[i + 3] : W[i + 2];
+        lo[i] = (q & 2) ? b2 : a;
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) w[i] = __funnelshift_r(lo[i], lo[i + 1], fs);
+}
+
 }  // namespace wlcs

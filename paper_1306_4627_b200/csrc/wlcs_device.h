@@ -21,10 +21,9 @@ struct BatchDev {
     const uint32_t* ids;   // optional: entry i is pair ids[i] (nullptr: pair i)
     int pm_bytes;          // shared-memory bytes for match masks per warp
     int kmax;              // largest words-per-lane K of a lane shape (<= 12)
+    int long_to_host;      // 1: pairs wider than 32 * kmax words are skipped (the host
+                           // runs them through the strip kernel); 0: second pass
     // filled by batch_launch from the workspace
-    uint32_t* keys_in;
-    uint32_t* vals_in;
-    uint32_t* keys;
     uint32_t* vals;
     uint32_t* meta;
     uint32_t* overflow;
@@ -38,6 +37,33 @@ cudaError_t batch_launch(BatchDev d, void* workspace, int sms, cudaStream_t stre
 cudaError_t int_peak_probe(int reps, double* ops_per_s, uint32_t* scratch);
 uint32_t* batch_overflow_count_ptr(void* workspace, uint32_t pairs);
 uint32_t* batch_overflow_list_ptr(void* workspace, uint32_t pairs);
+
+// Second pass (bitpar_wide.cu): the first pass's overflow list, finished on
+// the device at one word per lane with the 257-code mask table; pairs wider
+// than 32 words sweep 1024-column blocks with carries through `carry`.
+struct WideDev {
+    const uint8_t* xs;
+    const uint64_t* xoff;
+    uint64_t xs_bytes;
+    const uint8_t* ys;
+    const uint64_t* yoff;
+    uint64_t ys_bytes;
+    uint32_t* out;
+    const uint32_t* list;   // pair ids (the first pass's overflow list)
+    const uint32_t* count;  // device count of list entries (<= cap)
+    uint32_t cap;
+    uint32_t pairs_total;   // pairs of the whole batch (carry-slot layout)
+    uint16_t* carry[2];     // wide_scratch_words() words each (ping-pong)
+    const uint4* safe16;    // 16 zero bytes in device memory
+    // filled by wide_launch from the workspace
+    uint32_t* meta;
+    uint32_t* vals;
+    uint32_t* bucket;
+    uint32_t* rank;
+};
+size_t wide_workspace_bytes(uint32_t cap);
+size_t wide_scratch_words(uint64_t xs_bytes, uint64_t ys_bytes, uint32_t pairs);
+cudaError_t wide_launch(WideDev d, void* workspace, int sms, cudaStream_t stream);
 
 }  // namespace wlcs
 
@@ -69,17 +95,26 @@ struct FillProblem {
     uint32_t* ext_out;
 };
 
-// One strip-kernel launch: 1 or 2 problems sharing the column alphabet.
+// One strip-kernel launch: up to kMaxProblems problems sharing the column
+// alphabet (1 = plain fill, 2 = bidirectional split, 2G = the column split of
+// G slices played inside one launch).  CTA b serves problem b % nprob only and
+// takes that problem's strips from ticket[b % nprob] in increasing order, so
+// every problem has its own pool of warps: a strip waits only on an earlier
+// strip of its own pool (already running) or on the neighbouring slice's last
+// strip, whose pool is never starved by this one (liveness with more strips
+// than resident warps).
+constexpr int kMaxProblems = 8;
 struct PairDev {
-    FillProblem prob[2];
+    FillProblem prob[kMaxProblems];
     int nprob;
     uint32_t code_stride;   // smem bytes per code record (set by pair_fill)
     uint32_t pm_warp_bytes; // smem bytes of the match masks (set by pair_fill)
-    int carry_ahead;        // carry-word groups staged ahead (1 or 2; set by pair_fill)
+    int max_ctas;           // optional grid cap (0 = resident warps); tests force pools < strips
     const uint8_t* colp0;   // column string of problem 0 (alphabet scan)
     const uint16_t* map;    // 256 byte -> code map of the column alphabet
     int sigma;              // codes incl. the zero row
-    uint32_t* ticket;       // strip ticket counter
+    uint32_t* ticket;       // per-problem strip ticket counters [kMaxProblems], zeroed
+    uint32_t* error;        // zeroed; set when a carry poll times out (watchdog)
     uint32_t* sink;         // scratch the strip kernel's non-publishing lanes store to
                             // (>= kPairSinkWords words)
     const uint4* safe16;    // 16 zero bytes in device memory

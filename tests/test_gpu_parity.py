@@ -4,6 +4,8 @@ Bit-exact for every length and every recovered subsequence (integer/byte
 work: no tolerance).  Mirrors the reference's own tests:
 proj/tests/test_core.cpp, test_kernels.cpp, test_parallel.cpp, acceptance.cpp.
 """
+import ctypes
+
 import numpy as np
 import pytest
 
@@ -517,3 +519,121 @@ def test_batch_every_lane_shape(wl, restatement, alphabet):
                     xs.append(r); ys.append(c)
     xr, yr = rand_pairs(rng, 1500, 1, 1400, alphabet)
     check_batch(wl, restatement, xs + xr, ys + yr)
+
+
+# ---- round 2: device second pass, caller-stream ordering, column-split liveness
+
+def _device_batch(wl, xs, ys, stream=None, tight=False):
+    import torch
+    xb, xo, yb, yo = wl.pack_pairs(xs, ys)
+    dev = torch.device("cuda", 0)
+    pad = np.zeros(0 if tight else 16, np.uint8)
+    d_xs = torch.from_numpy(np.concatenate([xb, pad])).to(dev)
+    d_ys = torch.from_numpy(np.concatenate([yb, pad])).to(dev)
+    d_xo = torch.from_numpy(xo.view(np.int64)).to(dev)
+    d_yo = torch.from_numpy(yo.view(np.int64)).to(dev)
+    d_out = torch.full((len(xs),), -1, dtype=torch.int32, device=dev)
+    s = stream if stream is not None else torch.cuda.current_stream()
+    wl.lcs_length_batch_device(d_xs.data_ptr(), d_xo.data_ptr(), d_ys.data_ptr(), d_yo.data_ptr(),
+                               len(xs), int(xo[-1]), int(yo[-1]), d_out.data_ptr(), s.cuda_stream)
+    return (xb, xo, yb, yo), d_out, s
+
+
+def test_batch_device_wide_pairs_second_pass(wl, restatement):
+    """The device entry point has no host fallback: pairs wider than the first
+    pass's lane shapes (shorter string > 10,240 bytes) and byte alphabets with
+    all 256 values in one 1024-column block (257 codes) are finished by the
+    device second pass in column blocks (bitpar_wide.cu)."""
+    import torch
+    rng = np.random.default_rng(2026)
+    a = np.arange(256, dtype=np.uint8)
+    xs, ys = [], []
+    for k in range(40):
+        m = int(rng.integers(10000, 26000))
+        n = int(rng.integers(10241, 21000))
+        alpha = a if k % 2 else np.frombuffer(DNA, np.uint8)
+        xs.append(alpha[rng.integers(0, len(alpha), m)].tobytes())
+        ys.append(alpha[rng.integers(0, len(alpha), n)].tobytes())
+    for _ in range(300):  # 1024-4096 columns, every byte value present
+        m, n = int(rng.integers(1024, 4097)), int(rng.integers(1024, 4097))
+        xs.append(a[rng.integers(0, 256, m)].tobytes())
+        ys.append(np.concatenate([a, a[rng.integers(0, 256, n - 256)]])[rng.permutation(n)].tobytes())
+    for _ in range(200):  # mixed with ordinary first-pass pairs
+        m, n = int(rng.integers(1, 900)), int(rng.integers(1, 900))
+        xs.append(rng.choice(np.frombuffer(PROTEIN, np.uint8), m).tobytes())
+        ys.append(rng.choice(np.frombuffer(PROTEIN, np.uint8), n).tobytes())
+    (xb, xo, yb, yo), d_out, _ = _device_batch(wl, xs, ys)
+    torch.cuda.synchronize()
+    want = restatement.length_batch(xb, xo, yb, yo)
+    got = d_out.cpu().numpy().astype(np.uint32)
+    bad = np.nonzero(got != want)[0]
+    assert bad.size == 0, f"{bad.size} mismatches, first {bad[0]}: {got[bad[0]]} vs {want[bad[0]]}"
+    # the host entry point routes the wide pairs to the strip kernel instead
+    assert np.array_equal(wl.lcs_length_batch(xb, xo, yb, yo), want)
+
+
+def test_batch_device_is_ordered_on_caller_stream(wl, restatement):
+    """Asynchronous device entry on a side stream: inputs written by a kernel
+    on that stream just before the call, and the output read after it on the
+    same stream, without any host synchronisation in between."""
+    import torch
+    rng = np.random.default_rng(77)
+    xs, ys = rand_pairs(rng, 4000, 100, 1000, PROTEIN)
+    xb, xo, yb, yo = wl.pack_pairs(xs, ys)
+    dev = torch.device("cuda", 0)
+    side = torch.cuda.Stream(device=dev)
+    with torch.cuda.stream(side):
+        d_xs = torch.zeros(len(xb) + 16, dtype=torch.uint8, device=dev)
+        d_ys = torch.zeros(len(yb) + 16, dtype=torch.uint8, device=dev)
+        d_xs[: len(xb)].copy_(torch.from_numpy(xb), non_blocking=False)
+        d_ys[: len(yb)].copy_(torch.from_numpy(yb), non_blocking=False)
+        d_xo = torch.from_numpy(xo.view(np.int64)).to(dev)
+        d_yo = torch.from_numpy(yo.view(np.int64)).to(dev)
+        d_out = torch.full((len(xs),), -1, dtype=torch.int32, device=dev)
+        wl.lcs_length_batch_device(d_xs.data_ptr(), d_xo.data_ptr(), d_ys.data_ptr(),
+                                   d_yo.data_ptr(), len(xs), len(xb), len(yb), d_out.data_ptr(),
+                                   side.cuda_stream)
+        res = d_out.to(torch.int64) + 0  # consumer kernel on the same stream
+    side.synchronize()
+    assert np.array_equal(res.cpu().numpy().astype(np.uint32),
+                          restatement.length_batch(xb, xo, yb, yo))
+
+
+def test_length_device_honours_stream(wl, restatement):
+    import torch
+    rng = np.random.default_rng(5)
+    x = rng.choice(np.frombuffer(DNA, np.uint8), 30000).tobytes()
+    y = rng.choice(np.frombuffer(DNA, np.uint8), 20000).tobytes()
+    dev = torch.device("cuda", 0)
+    side = torch.cuda.Stream(device=dev)
+    with torch.cuda.stream(side):
+        d_x = torch.zeros(len(x) + 16, dtype=torch.uint8, device=dev)
+        d_y = torch.zeros(len(y) + 16, dtype=torch.uint8, device=dev)
+        torch.cuda._sleep(20_000_000)  # keep the side stream busy before the copies land
+        d_x[: len(x)].copy_(torch.from_numpy(np.frombuffer(x, np.uint8)))
+        d_y[: len(y)].copy_(torch.from_numpy(np.frombuffer(y, np.uint8)))
+        out = ctypes.c_uint32()
+        wl._check(wl.lib.wlcs_length_device(d_x.data_ptr(), len(x), d_y.data_ptr(), len(y),
+                                            wl.VARIANT_BITPARALLEL, ctypes.byref(out),
+                                            side.cuda_stream))
+    assert out.value == restatement.length_bitpar(x, y)
+
+
+@pytest.mark.parametrize("slices,max_ctas", [(2, 4), (3, 6), (4, 8), (4, 16), (2, 0), (4, 0)])
+def test_colsplit_slices_run_concurrently(wl, restatement, slices, max_ctas):
+    """The column split's fused hand-off with every slice's producer and
+    consumer RUNNING AT THE SAME TIME (one launch, one CTA pool per slice and
+    direction) and -- for max_ctas > 0 -- far fewer warps per pool than strips
+    per problem: the liveness case of the shared-ticket design."""
+    rng = np.random.default_rng(slices * 100 + max_ctas)
+    x = rng.choice(np.frombuffer(DNA, np.uint8), 6000).tobytes()
+    y = rng.choice(np.frombuffer(DNA, np.uint8), 180_000).tobytes()
+    assert wl.colsplit_emulate(x, y, slices, max_ctas) == restatement.length_bitpar(x, y)
+
+
+def test_colsplit_concurrent_byte_alphabet(wl, restatement):
+    rng = np.random.default_rng(9)
+    a = np.arange(256, dtype=np.uint8)
+    x = a[np.minimum(rng.zipf(1.1, 5000), 256) - 1].tobytes()
+    y = a[np.minimum(rng.zipf(1.1, 70_000), 256) - 1].tobytes()
+    assert wl.colsplit_emulate(x, y, 3, 6) == restatement.length_bitpar(x, y)

@@ -189,3 +189,27 @@ def test_colsplit_combine_single_process():
             cin = res.strip_rows(x[mid:][::-1], y[lo:hi][::-1], v, cin)
             vrs[g] = v
         assert multigpu.colsplit_combine(bounds, vfs, vrs, len(y)) == want, world
+
+
+def test_bench_two_ranks_shard_the_c2_batch():
+    """`bench.py --gpus 2` without WORLD_SIZE re-launches itself under
+    torch.distributed.run (2 ranks, gloo); the two ranks' shards cover the
+    configured 65,536-pair batch exactly once (strong scaling).  --dry-run
+    stops before device work, so this runs on the CPU."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, WLCS_DIST_BACKEND="gloo", WLCS_BENCH_ONE_DEVICE="1")
+    env.pop("WORLD_SIZE", None)
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--dry-run"],
+                       capture_output=True, text=True, timeout=600, env=env, cwd=root)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    rec = json.loads(lines[0])
+    assert rec["n_gpus"] == 2 and rec["scaling"] == "strong"
+    assert rec["pairs_total"] == 65536
+    assert rec["cells_total"] == rec["cells_batch"]
+    # balanced by cells: neither rank holds much more than half
+    assert rec["max_rank_cells"] <= 0.51 * rec["cells_batch"]

@@ -193,3 +193,49 @@ def test_capacity_formula_matches_reference():
         except oracle.ReferenceError_ as e:
             raised = e.kind == "CapacityError"
         assert raised == res.capacity_exceeded(m, n, budget), (m, n, budget)
+
+
+def test_oracle_generate_pairs_matches_library(restatement):
+    """The reference arm of bench.py builds its C2 inputs with the oracle's
+    restatement of the generator (it must not load the product library);
+    both must produce the same bytes."""
+    import ctypes
+
+    import paper_1306_4627_b200 as wl
+    P = 2000
+    xs, xo, ys, yo = restatement.generate_pairs(P, 200, 1000, b"ACDEFGHIKLMNPQRSTVWY", 20130619)
+    a = np.frombuffer(b"ACDEFGHIKLMNPQRSTVWY", np.uint8)
+    xs2, ys2 = np.empty(P * 1000, np.uint8), np.empty(P * 1000, np.uint8)
+    xo2, yo2 = np.empty(P + 1, np.uint64), np.empty(P + 1, np.uint64)
+    u64p = ctypes.POINTER(ctypes.c_uint64)
+    wl._check(wl.lib.wlcs_generate_pairs(ctypes.c_size_t(P), ctypes.c_size_t(200),
+                                         ctypes.c_size_t(1000), a.ctypes.data, ctypes.c_size_t(20),
+                                         ctypes.c_uint64(20130619), xs2.ctypes.data,
+                                         xo2.ctypes.data_as(u64p), ys2.ctypes.data,
+                                         yo2.ctypes.data_as(u64p)))
+    assert np.array_equal(xo, xo2) and np.array_equal(yo, yo2)
+    assert np.array_equal(xs[: xo[-1]], xs2[: xo2[-1]]) and np.array_equal(ys[: yo[-1]], ys2[: yo2[-1]])
+
+
+def test_cells_mt_equals_two_row_loop(restatement):
+    """The multi-threaded two-row lcs_cell loop used for the full-size C4/C5
+    goldens (SURVEY.md 8(c) check (i)) against the one-thread loop."""
+    rng = np.random.default_rng(17)
+    for t in range(60):
+        m, n = int(rng.integers(0, 400)), int(rng.integers(0, 400))
+        k = int(rng.integers(1, 6))
+        x = bytes(rng.integers(65, 65 + k, m).astype(np.uint8))
+        y = bytes(rng.integers(65, 65 + k, n).astype(np.uint8))
+        assert restatement.length_cells_mt(x, y, int(rng.integers(1, 9))) == restatement.length_cells(x, y)
+
+
+def test_large_goldens_two_oracles_agree():
+    """at the full C4 / C5 sizes (which the reference cannot
+    run: 5 TB of tables) the two-row lcs_cell loop (i) and the 64-bit Hyyro
+    length (ii) agree (tests/golden/make_large_golden*.py)."""
+    import json
+    import os
+    with open(os.path.join(os.path.dirname(__file__), "golden", "large_configs.json")) as f:
+        g = json.load(f)
+    for name in ("c4", "c5"):
+        assert g[name]["lcs_length_cells"] == g[name]["lcs_length"], name
