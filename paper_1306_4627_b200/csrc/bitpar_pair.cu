@@ -124,12 +124,14 @@ __device__ __forceinline__ uint4 ld_relaxed_sys_v4(const uint32_t* p) {
                  : "memory");
     return v;
 }
+// gpu-scope relaxed vector load of four carry words (a strong load: the
+// producer's relaxed stores and this poll do not race).  No "memory" clobber:
+// the words validate themselves, so other accesses may move across the poll.
 __device__ __forceinline__ uint4 ld_relaxed_gpu_v4(const uint32_t* p) {
     uint4 v;
     asm volatile("ld.relaxed.gpu.global.v4.u32 {%0, %1, %2, %3}, [%4];"
                  : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-                 : "l"(p)
-                 : "memory");
+                 : "l"(p));
     return v;
 }
 
@@ -201,8 +203,8 @@ __global__ void pair_code_rows_kernel(const uint8_t* row, int64_t rows, int reve
 // is needed.  Strip s+1 reads the words four chunks at a time with one 16-byte
 // relaxed load (gpu scope; sys scope for a neighbour GPU's inbox), the same
 // address for the whole warp: a broadcast, so the hand-off code is
-// warp-uniform.  The load of group g+1 is issued when group g is consumed; a
-// group with a word still 0 is re-polled.  Inside the warp the carry masks
+// warp-uniform.  The load of group g+1 is issued half way through group g;
+// a group with a word still 0 is re-polled.  Inside the warp the carry masks
 // move with two shuffles per step (rows 0-7 after row 7, rows 8-15 after row
 // 15), so the shuffle latency hides behind row work.
 //
@@ -276,9 +278,8 @@ __global__ void __launch_bounds__(32, 1) pair_strip_kernel(PairDev d) {
         for (int j = 0; j < kCodeAhead; ++j) ring[j] = load_codes(cp + j * cstride);
         cp += kCodeAhead * cstride;
         // the left strip's carry words: group g+1 (chunks 4g+4 .. 4g+7) is
-        // loaded when group g is consumed -- a whole group of steps ahead, so
-        // the load has landed when its value is moved (carry rows are padded
-        // by 16 words past the last chunk)
+        // loaded at step 2 of group g, two steps before its value is moved
+        // (carry rows are padded by 16 words past the last chunk)
         uint4 cw = make_uint4(0, 0, 0, 0);
         uint4 cw_next = feeder ? carry_ld4(left_carry) : make_uint4(0, 0, 0, 0);
         const uint8_t* pml = pm + lane_off;
@@ -302,13 +303,17 @@ __global__ void __launch_bounds__(32, 1) pair_strip_kernel(PairDev d) {
                         return;
                     }
                 }
-                cw_next = carry_ld4(left_carry + tg + 4);
                 prefetch_l2(left_carry + tg + 16);
             }
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 const int t = tg + j;
                 const int ch = t - int(lane);
+                // the next group's carry words are loaded half way through this
+                // group: two steps ahead of their use, yet fresh enough that they
+                // are usually published (measured: loading them at the group start
+                // found them stale and cost C4 +22%, re-polling synchronously)
+                if (j == 2 && feeder && tg < nchunks) cw_next = carry_ld4(left_carry + tg + 4);
                 if (lane == 0) {
                     uint32_t fl = j == 0 ? cw.x : j == 1 ? cw.y : j == 2 ? cw.z : cw.w;
                     if (t >= nchunks) fl = 0;  // padding rows take no carry

@@ -32,6 +32,7 @@ constexpr int kWmTaskStart = 0;
 constexpr int kWmPairStart = 8;
 constexpr int kWmCount = 16;
 constexpr int kWmTicket = 24;
+constexpr int kWmSafe16 = 28;  // 16 zero bytes (chunk loads with no valid byte)
 constexpr int kWmWords = 32;
 // shared memory per warp: map u16[256] | inv u16[16] (+pad) | masks [257][32 lanes]
 constexpr uint32_t kWideMapBytes = 1024;
@@ -136,6 +137,7 @@ __global__ void __launch_bounds__(1024) wide_plan_kernel(WideDev d) {
         }
         d.meta[kWmTaskStart + kWideOrders] = ts;
         d.meta[kWmTicket] = 0;
+        for (int k = 0; k < 4; ++k) d.meta[kWmSafe16 + k] = 0;
     }
 }
 
@@ -322,6 +324,7 @@ size_t wide_scratch_words(uint64_t xs_bytes, uint64_t ys_bytes, uint32_t pairs) 
 cudaError_t wide_launch(WideDev d, void* workspace, int sms, cudaStream_t stream) {
     uint32_t* ws = static_cast<uint32_t*>(workspace);
     d.meta = ws;
+    d.safe16 = reinterpret_cast<const uint4*>(ws + kWmSafe16);  // zeroed by the planner
     d.vals = ws + kWmWords;
     d.bucket = d.vals + d.cap;
     d.rank = d.bucket + d.cap;

@@ -54,8 +54,8 @@ struct WideDev {
     uint32_t cap;
     uint32_t pairs_total;   // pairs of the whole batch (carry-slot layout)
     uint16_t* carry[2];     // wide_scratch_words() words each (ping-pong)
-    const uint4* safe16;    // 16 zero bytes in device memory
     // filled by wide_launch from the workspace
+    const uint4* safe16;    // 16 zero bytes in device memory
     uint32_t* meta;
     uint32_t* vals;
     uint32_t* bucket;
