@@ -13,9 +13,9 @@ CLI := paper_1306_4627_b200/_lib/wavelcs_b200
 CU_SRCS := $(wildcard $(SRC)/*.cu)
 CXX_SRCS := $(wildcard $(SRC)/*.cpp)
 OBJS := $(patsubst $(SRC)/%.cu,$(OBJ)/%.o,$(CU_SRCS)) $(patsubst $(SRC)/%.cpp,$(OBJ)/%.cpp.o,$(CXX_SRCS))
-HDRS := $(wildcard $(SRC)/*.cuh) $(wildcard $(SRC)/*.h) $(wildcard include/*.h) $(wildcard include/*.hpp)
+HDRS := $(wildcard $(SRC)/*.cuh) $(wildcard $(SRC)/*.h) $(wildcard include/*.h) $(wildcard include/*.hpp) $(wildcard include/wavelcs/*.hpp)
 
-all: lib oracle $(FACADE_TEST) $(CLI)
+all: lib oracle $(FACADE_TEST) $(CLI) reftests
 
 lib: $(LIB)
 
@@ -48,7 +48,12 @@ $(LIB): $(OBJS)
 oracle:
 	$(MAKE) -s -C oracle
 
+# the reference's unit tests and acceptance suite, compiled unchanged against
+# include/wavelcs/ (only where /root/reference exists; prebuilt elsewhere)
+reftests: $(LIB) $(CLI)
+	$(MAKE) -s -C tests/cpp
+
 clean:
 	rm -rf build $(LIB) $(FACADE_TEST) $(CLI)
 
-.PHONY: all lib oracle clean
+.PHONY: all lib oracle reftests clean

@@ -196,6 +196,17 @@ int wlcs_colsplit_fill(const uint8_t* x, size_t m, const uint8_t* y, size_t n, s
 int wlcs_fill_tables(const uint8_t* x, size_t m, const uint8_t* y, size_t n,
                      size_t memory_budget, uint32_t* dp, uint8_t* back);
 
+/* The reference's block-kernel plugin contract (BlockArgs,
+ * include/wavelcs/kernels.hpp:23-35 of the reference; compute_block,
+ * parallel.hpp:78-79): fill cells [i_first, i_last] x [j_first, j_last]
+ * (1-based, inclusive) of the caller's HOST tables -- c: DP cells
+ * c[i * c_stride + j], b: arrows b[(i-1) * b_stride + (j-1)] -- from their
+ * final row i_first - 1 and column j_first - 1, on the device, with
+ * lcs_cell's values and arrows.  x[i-1] / y[j-1] are the i-th / j-th
+ * symbols.  An empty range is a no-op. */
+int wlcs_fill_block(const uint8_t* x, const uint8_t* y, uint32_t* c, size_t c_stride, uint8_t* b,
+                    size_t b_stride, size_t i_first, size_t i_last, size_t j_first, size_t j_last);
+
 /* Single-process multi-GPU conveniences, devices 0..n_gpus-1
  * of the calling process, one host thread per device:
  *  - wlcs_length_batch_multi: pairs sharded into contiguous ranges balanced by

@@ -94,7 +94,7 @@ struct Ctx {
     // batch (ws: first pass per chunk; ws2 + wcarry: the device second pass)
     DevBuf xs, ys, xoff, yoff, out, ws, ws2, wcarry;
     // single pair
-    DevBuf px, py, pmg, carry, small, rows, outrev, codes, ry, vbuf, wave, sink, walk;
+    DevBuf px, py, pmg, carry, small, rows, outrev, codes, ry, vbuf, wave, sink, walk, tile;
     ~Ctx() {
         if (hscratch) cudaFreeHost(hscratch);
         for (cudaEvent_t e : chunk_ev) cudaEventDestroy(e);
@@ -1445,6 +1445,50 @@ int wlcs_fill_tables(const uint8_t* x, size_t m, const uint8_t* y, size_t n,
     WLCS_CUDA(cudaMemcpyAsync(dp, tdp.p, dp_bytes, cudaMemcpyDeviceToHost, c->stream));
     WLCS_CUDA(cudaMemcpyAsync(back, tback.p, back_bytes, cudaMemcpyDeviceToHost, c->stream));
     WLCS_CUDA(stream_wait(c->stream));
+    return WLCS_OK;
+}
+
+// ------------------------------------------------- block-kernel contract
+int wlcs_fill_block(const uint8_t* x, const uint8_t* y, uint32_t* c, size_t c_stride, uint8_t* b,
+                    size_t b_stride, size_t i_first, size_t i_last, size_t j_first, size_t j_last) {
+    if (i_last < i_first || j_last < j_first) return WLCS_OK;  // empty tile
+    if (!x || !y || !c || !b) return fail(WLCS_E_INVALID_ARGUMENT, "NULL argument");
+    if (i_first == 0 || j_first == 0)
+        return fail(WLCS_E_OUT_OF_RANGE, "block cell ranges are 1-based");
+    if (j_last >= c_stride || j_last > b_stride)
+        return fail(WLCS_E_OUT_OF_RANGE, "block columns exceed the table stride");
+    const size_t h = i_last - i_first + 1, w = j_last - j_first + 1;
+    if (h > size_t(INT32_MAX) || w > size_t(INT32_MAX))
+        return fail(WLCS_E_INVALID_ARGUMENT, "block too large");
+    Ctx* ctx = nullptr;
+    int rc = get_ctx(&ctx);
+    if (rc) return rc;
+    // borders: north row (corner first) and west column, packed after the symbols
+    std::vector<uint32_t> border(w + 1 + h);
+    for (size_t k = 0; k <= w; ++k) border[k] = c[(i_first - 1) * c_stride + (j_first - 1) + k];
+    for (size_t r = 0; r < h; ++r) border[w + 1 + r] = c[(i_first + r) * c_stride + (j_first - 1)];
+    const size_t sym = ((h + w) + 15) & ~size_t(15);
+    const size_t cells = h * w;
+    WLCS_CUDA(ctx->tile.ensure(sym + border.size() * 4 + cells * 5 + 64));
+    uint8_t* base = ctx->tile.as<uint8_t>();
+    uint32_t* d_border = reinterpret_cast<uint32_t*>(base + sym);
+    uint32_t* d_cv = d_border + border.size();
+    uint8_t* d_bv = reinterpret_cast<uint8_t*>(d_cv + cells);
+    cudaStream_t s = ctx->stream;
+    WLCS_CUDA(cudaMemcpyAsync(base, x + (i_first - 1), h, cudaMemcpyHostToDevice, s));
+    WLCS_CUDA(cudaMemcpyAsync(base + h, y + (j_first - 1), w, cudaMemcpyHostToDevice, s));
+    WLCS_CUDA(cudaMemcpyAsync(d_border, border.data(), border.size() * 4, cudaMemcpyHostToDevice, s));
+    WLCS_CUDA(wlcs::tile_fill(base, base + h, d_border, d_border + w + 1, d_cv, d_bv, int(h),
+                              int(w), s));
+    std::vector<uint32_t> cv(cells);
+    std::vector<uint8_t> bv(cells);
+    WLCS_CUDA(cudaMemcpyAsync(cv.data(), d_cv, cells * 4, cudaMemcpyDeviceToHost, s));
+    WLCS_CUDA(cudaMemcpyAsync(bv.data(), d_bv, cells, cudaMemcpyDeviceToHost, s));
+    WLCS_CUDA(stream_wait(s));
+    for (size_t r = 0; r < h; ++r) {
+        std::memcpy(c + (i_first + r) * c_stride + j_first, cv.data() + r * w, w * 4);
+        std::memcpy(b + (i_first + r - 1) * b_stride + (j_first - 1), bv.data() + r * w, w);
+    }
     return WLCS_OK;
 }
 

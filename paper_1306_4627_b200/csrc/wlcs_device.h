@@ -174,6 +174,13 @@ struct WavePairDev {
     uint32_t* out;        // LCS length
 };
 
+// ---- the reference's block-kernel contract on the device (tiles.cu) ----
+// Tile of h x w cells from its north row (w + 1 values, corner first) and
+// west column (h values); cv / bv receive the tile's cells and arrows.
+cudaError_t tile_fill(const uint8_t* d_x, const uint8_t* d_y, const uint32_t* d_north,
+                      const uint32_t* d_west, uint32_t* d_cv, uint8_t* d_bv, int h, int w,
+                      cudaStream_t stream);
+
 size_t wave_batch_smem();
 cudaError_t wave_batch_launch(const WaveBatchDev& d, int sms, cudaStream_t stream);
 int64_t wave_pair_bands(int64_t m);

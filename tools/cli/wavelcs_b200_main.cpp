@@ -1,11 +1,12 @@
 // wavelcs_b200 -- command-line front end on the GPU path (SURVEY.md 8(f)
 // rank 2), mirroring the reference's tools/wavelcs_main.cpp subcommands and
 // output lines (compute: "LCS length:", "Similarity:", "Fill time:", "LCS:";
-// bench: the reference CSV header extended with device GCUPS; gen).  The
+// bench: the reference's cases, equivalence gate and 8-column CSV, or with
+// --gcups the device throughput / roofline schema; gen).  The
 // reference's CLI11 is not vendored, so arguments are parsed here.  Every
 // computation goes through the C++ facade (include/wavelcs_b200.hpp) and thus
-// the device; --workers / --block-size / --kernel are accepted for command-
-// line compatibility and have no effect on the device path.
+// the device; --workers / --block-size / --kernel are validated as the
+// reference validates them and otherwise do not change the device path.
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -13,6 +14,7 @@
 #include <fstream>
 #include <iostream>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "wavelcs_b200.hpp"
@@ -50,6 +52,13 @@ InputFormat pick_format(const std::string& flag, const std::string& path) {
     return format_from_path(path);
 }
 
+KernelKind parse_kernel(const std::string& name) {
+    for (KernelKind k : {KernelKind::Auto, KernelKind::Scalar, KernelKind::Avx2, KernelKind::Neon,
+                         KernelKind::B200})
+        if (name == kernel_name(k)) return k;
+    throw ConfigError("--kernel must be one of auto, scalar, avx2, neon, b200; got '" + name + "'");
+}
+
 int run_compute(Args& a) {
     std::string parent, child, format;
     bool with_tb = false, validate = false;
@@ -63,7 +72,11 @@ int run_compute(Args& a) {
             if (format != "plain" && format != "fasta")
                 throw ConfigError("--format must be plain or fasta");
         } else if (o == "--validate-dna") validate = true;
-        else if (o == "--workers" || o == "--block-size" || o == "--kernel") (void)a.next(o);
+        else if (o == "--workers") {
+            if (std::stoul(a.next(o)) == 0) throw ConfigError("worker count must be at least 1");
+        } else if (o == "--block-size") {
+            if (std::stoull(a.next(o)) == 0) throw ConfigError("block size must be at least 1");
+        } else if (o == "--kernel") (void)resolve_kernel(parse_kernel(a.next(o)));
         else throw ConfigError("unknown option " + o);
     }
     if (parent.empty() || child.empty()) throw ConfigError("compute needs --parent and --child");
@@ -88,48 +101,36 @@ int run_compute(Args& a) {
     return 0;
 }
 
-int run_bench(Args& a) {
-    std::vector<std::string> sizes;
-    std::string out_path;
-    std::uint64_t seed = 1;
-    unsigned reps = 3;
-    while (a.more()) {
-        const std::string o = a.next("");
-        if (o == "--sizes") {
-            for (const auto& s : split(a.next(o), ',')) sizes.push_back(s);
-        } else if (o == "--seed") seed = std::stoull(a.next(o));
-        else if (o == "--repetitions") {
-            reps = unsigned(std::stoul(a.next(o)));
-            if (reps == 0) throw ConfigError("--repetitions must be positive");
-        } else if (o == "--out") out_path = a.next(o);
-        else if (o == "--workers" || o == "--block-size" || o == "--kernel") (void)a.next(o);
-        else throw ConfigError("unknown option " + o);
+std::pair<size_t, size_t> parse_size(const std::string& st) {
+    const size_t xpos = st.find_first_of("xX");
+    if (xpos == std::string::npos || xpos == 0 || xpos + 1 >= st.size())
+        throw ConfigError("--sizes entries must look like MxN, got '" + st + "'");
+    try {
+        return {std::stoull(st.substr(0, xpos)), std::stoull(st.substr(xpos + 1))};
+    } catch (const std::exception&) {
+        throw ConfigError("--sizes entries must look like MxN, got '" + st + "'");
     }
-    if (sizes.empty()) throw ConfigError("bench needs --sizes");
-    if (out_path.empty()) throw ConfigError("bench needs --out");
+}
+
+// --gcups: device throughput per size (bit-parallel length fill, best of R),
+// the GPU variants' equivalence gate, and the fraction of the measured int
+// roofline -- the B200 measurement; the default mode is the reference's.
+int run_bench_gcups(const std::vector<std::pair<size_t, size_t>>& sizes, std::uint64_t seed,
+                    unsigned reps, const std::string& out_path) {
     std::ofstream out(out_path, std::ios::trunc);
     if (!out) throw InputError("cannot open '" + out_path + "' for writing");
     out << "# wavelcs_b200 benchmark (device: B200, bit-parallel fill)\n";
     out << "# generator: mt19937_64, symbol = alphabet[next() % |alphabet|], alphabet=ACGT\n";
     out << "# seeds: parent = seed, child = seed + 0x9e3779b97f4a7c15\n";
-    // roofline denominator: the device's measured int32 ALU peak, 3 ops per
-    // 32-cell word-row
     double peak_ops = 0.0;
     if (wlcs_probe_int_peak(3, &peak_ops) != WLCS_OK) throw DeviceError(wlcs_last_error());
     const double gcups_peak = peak_ops * 32.0 / 3.0 / 1e9;
     out << "# int roofline: " << gcups_peak << " GCUPS (measured int32 ALU peak x 32/3)\n";
     out << "M,N,repetitions,device_s,gcups,roofline_frac,lcs_length\n";
-    size_t n_rec = 0;
-    for (const auto& st : sizes) {
-        const size_t xpos = st.find_first_of("xX");
-        if (xpos == std::string::npos || xpos == 0 || xpos + 1 >= st.size())
-            throw ConfigError("--sizes entries must look like MxN, got '" + st + "'");
-        const size_t m = std::stoull(st.substr(0, xpos)), n = std::stoull(st.substr(xpos + 1));
+    for (const auto& [m, n] : sizes) {
         const Sequence x = generate_random(m, Sequence("ACGT"), seed);
-        const Sequence y = generate_random(n, Sequence("ACGT"), seed + 0x9e3779b97f4a7c15ull);
+        const Sequence y = generate_random(n, Sequence("ACGT"), seed + kChildSeedOffset);
         Length len = lcs_length(x, y, kNoMemoryBudget);  // warm-up
-        // equivalence gate (bench.cpp:100-106 semantics): the two device
-        // fill variants must agree
         std::uint32_t wave = 0;
         if (wlcs_length_ex(reinterpret_cast<const std::uint8_t*>(x.data()), m,
                            reinterpret_cast<const std::uint8_t*>(y.data()), n, WLCS_NO_BUDGET,
@@ -140,21 +141,71 @@ int run_bench(Args& a) {
                                    ": bit-parallel " + std::to_string(len) + " vs wavefront " +
                                    std::to_string(wave));
         double best = 1e300;
-        for (unsigned r = 0; r < reps; ++r) {
-            const auto t0 = std::chrono::steady_clock::now();
-            len = lcs_length(x, y, kNoMemoryBudget);
-            best = std::min(best, std::chrono::duration<double>(
-                                      std::chrono::steady_clock::now() - t0).count());
-        }
+        for (unsigned r = 0; r < reps; ++r)
+            best = std::min(best, time_fill([&] { len = lcs_length(x, y, kNoMemoryBudget); }));
         char line[256];
         const double gcups = double(m) * double(n) / best / 1e9;
-        std::snprintf(line, sizeof line, "%zu,%zu,%u,%.6f,%.1f,%.4f,%u\n", m, n, reps, best,
-                      gcups, gcups / gcups_peak, len);
+        std::snprintf(line, sizeof line, "%zu,%zu,%u,%.6f,%.1f,%.4f,%u\n", m, n, reps, best, gcups,
+                      gcups / gcups_peak, len);
         out << line;
         std::cout << line;
-        ++n_rec;
     }
-    std::cout << "wrote " << n_rec << " records to " << out_path << '\n';
+    std::cout << "wrote " << sizes.size() << " records to " << out_path << '\n';
+    return 0;
+}
+
+// The reference's bench subcommand (tools/wavelcs_main.cpp:110-139): the
+// cases (--sizes or --table1, crossed with --workers), run_benchmark with its
+// serial / parallel equivalence gate, and write_csv's 8-column schema.
+int run_bench(Args& a) {
+    std::vector<std::pair<size_t, size_t>> sizes;
+    std::vector<unsigned> workers;
+    std::string out_path;
+    std::uint64_t seed = 1;
+    unsigned reps = 3;
+    size_t block = kDefaultBlockSize;
+    bool table1 = false, gcups = false;
+    KernelKind kernel = KernelKind::Auto;
+    while (a.more()) {
+        const std::string o = a.next("");
+        if (o == "--sizes") {
+            for (const auto& st : split(a.next(o), ',')) sizes.push_back(parse_size(st));
+        } else if (o == "--table1") table1 = true;
+        else if (o == "--gcups") gcups = true;
+        else if (o == "--seed") seed = std::stoull(a.next(o));
+        else if (o == "--repetitions") {
+            reps = unsigned(std::stoul(a.next(o)));
+            if (reps == 0) throw ConfigError("--repetitions must be positive");
+        } else if (o == "--workers") {
+            for (const auto& w : split(a.next(o), ',')) workers.push_back(unsigned(std::stoul(w)));
+        } else if (o == "--block-size") block = std::stoull(a.next(o));
+        else if (o == "--kernel") kernel = parse_kernel(a.next(o));
+        else if (o == "--out") out_path = a.next(o);
+        else throw ConfigError("unknown option " + o);
+    }
+    if (out_path.empty()) throw ConfigError("bench needs --out");
+    if (sizes.empty() && !table1) throw ConfigError("bench needs --sizes or --table1");
+    if (gcups) {
+        if (table1)
+            for (const BenchCase& c : table1_cases(1, block, seed))
+                sizes.emplace_back(c.parent_len, c.child_len);
+        return run_bench_gcups(sizes, seed, reps, out_path);
+    }
+    if (workers.empty()) workers.push_back(default_worker_count());
+    std::vector<BenchCase> cases;
+    for (const unsigned w : workers) {
+        if (table1) {
+            for (const BenchCase& c : table1_cases(w, block, seed, reps)) cases.push_back(c);
+        } else {
+            for (const auto& [m, n] : sizes) cases.push_back({m, n, w, block, seed, reps});
+        }
+    }
+    BenchOptions options;
+    options.kernel = kernel;
+    options.progress = &std::cout;
+    const std::vector<BenchRecord> records = run_benchmark(cases, options);
+    write_csv(records, out_path);
+    std::cout << "wrote " << records.size() << " records to " << out_path << '\n';
     return 0;
 }
 
