@@ -46,10 +46,6 @@ constexpr int kTraceMax = 1 << 15;
 __device__ unsigned long long g_trace[kTraceMax][4];
 __device__ unsigned int g_trace_n;
 #endif
-#ifndef WLCS_BATCH_HALF_UNROLL
-#define WLCS_BATCH_HALF_UNROLL 1
-#endif
-constexpr int kHalfUnroll = WLCS_BATCH_HALF_UNROLL;  // half-chunk loop unroll (1: smaller code)
 constexpr int kNumClasses = 6 * kMaxK;   // S in {1,2,4,8,16,32} x K in 1..12
 constexpr int kChunkBuckets = 128;       // chunk-count buckets per class (clamped)
 constexpr int kBuckets = kNumClasses * kChunkBuckets;
@@ -660,10 +656,13 @@ __device__ __noinline__ int sweep_task_generic(const BatchDev& d, const LanePair
 }
 
 // Fast form (every lane's chunks lie inside its buffer): per step one
-// 16-byte load of the next chunk, 32-bit chunk classification, and the
-// byte -> code table switched to the all-zero table for chunks outside the
-// row string (identity rows); only the two partial chunks of a row string
-// are sanitized.  Shared memory is addressed through one 32-bit base.
+// 16-byte load of the next chunk and the row updates.  Only the edge steps
+// -- before every lane has reached its first full chunk, or after some lane
+// has passed its last one -- classify chunks: chunks outside a row string
+// read through the all-zero byte -> code table (identity rows) and the two
+// partial chunks of a string are sanitized; the steps in between (every
+// lane on a full chunk) skip all of it.  Shared memory is addressed through
+// one 32-bit base.
 template <bool CHAIN, int K>
 __device__ __forceinline__ int sweep_task(const BatchDev& d, const LanePair& p, int S, int s,
                                           const uint8_t* smem, uint32_t sbase, uint32_t zrep) {
@@ -682,6 +681,10 @@ __device__ __forceinline__ int sweep_task(const BatchDev& d, const LanePair& p, 
 #pragma unroll
     for (int k = 0; k < K; ++k) V[k] = 0xffffffffu;
     const int T = warp_max(nrch) + S - 1;
+    // steps [t_lo, t_hi): every lane's chunk t - s lies fully inside its string
+    // (chunks [a_r ? 1 : 0, (rows + a_r) / 16) are full)
+    const int t_lo = warp_max((a_r ? 1 : 0) + s);
+    const int t_hi = max(-warp_max(-(((rows + a_r) >> 4) + s)), t_lo);
     uint32_t cout = 0;
     int lo = -16 * s - a_r;  // row index of byte 0 of chunk ch = t - s
     const uint4* cptr = reinterpret_cast<const uint4*>(rstart);
@@ -699,17 +702,21 @@ __device__ __forceinline__ int sweep_task(const BatchDev& d, const LanePair& p, 
             cin <<= 16;
             cout = 0;
         }
-        const bool none = lo >= rows || lo <= -16;
-        const bool part = !none && (lo < 0 || lo > rows - 16);
-        if (__any_sync(kFullMask, part)) {
-            if (part) cur = sanitize_chunk(cur, valid_mask16(lo, rows), zrep);
+        uint32_t ma = map_a;
+        if (t < t_lo || t >= t_hi) {  // warp-uniform: an edge step
+            const bool none = lo >= rows || lo <= -16;
+            const bool part = !none && (lo < 0 || lo > rows - 16);
+            if (__any_sync(kFullMask, part)) {
+                if (part) cur = sanitize_chunk(cur, valid_mask16(lo, rows), zrep);
+            }
+            if (none) ma = zmap_a;
         }
-        const uint32_t ma = none ? zmap_a : map_a;
-#pragma unroll kHalfUnroll
+        uint32_t wlo = cur.x, whi = cur.y;
+#pragma unroll 1
         for (int h = 0; h < 2; ++h) {
-            const uint32_t wlo = h ? cur.z : cur.x;
-            const uint32_t whi = h ? cur.w : cur.y;
             rows8_sh<CHAIN, K>(V, ma, pm_a, wlo, whi, cin, cout);
+            wlo = cur.z;
+            whi = cur.w;
         }
         cur = nxt;
         lo += 16;
