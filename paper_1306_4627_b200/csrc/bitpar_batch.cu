@@ -36,9 +36,6 @@ namespace wlcs {
 namespace {
 
 constexpr int kMaxK = 12;
-#ifndef WLCS_BATCH_BUILD2
-#define WLCS_BATCH_BUILD2 1
-#endif
 #ifdef WLCS_BATCH_TRACE
 // Diagnostic build only (tools/trace_probe.py): per task the globaltimer at
 // its start and end, smid << 32 | build ns, (16 S + K) << 32 | max rows.
@@ -50,7 +47,11 @@ constexpr int kNumClasses = 6 * kMaxK;   // S in {1,2,4,8,16,32} x K in 1..12
 constexpr int kChunkBuckets = 128;       // chunk-count buckets per class (clamped)
 constexpr int kBuckets = kNumClasses * kChunkBuckets;
 constexpr int kTableSlots = (kNumClasses + 31) / 32;  // task-table entries per lane
-constexpr int kMapBytes = 512;  // map [256] + inverse code list [256]
+// per-warp shared memory before the masks: map [256] (byte -> code) | zmap [256]
+// (all zero: the map of chunks outside a row string) | inv [16 x u16] (low-
+// nibble presence per high nibble of the map's bytes) | pad
+constexpr int kMapBytes = 576;
+constexpr uint32_t kZmapOff = 256, kInvOff = 512;
 constexpr uint32_t kNoBucket = 0xffffffffu;
 
 // meta[] layout (uint32)
@@ -349,29 +350,38 @@ __device__ __forceinline__ TaskInfo decode_task(const TaskTable& tt, uint32_t t)
 // every code's match mask is the AND over the planes of "plane == bit of the
 // code's byte value": a handful of LOP3 per (code, word), written once --
 // no read-modify-write, no dependency chains, ALU only.
-// Builds the task's byte -> code map and match masks in shared memory.  K is
-// a runtime value and every loop over words / codes is rolled: the build is
-// one small piece of code shared by all lane shapes (it runs once per task
-// while the sweep code is hot, so its I-cache footprint matters).
+// The byte -> code map a warp keeps from one task to the next (hm == 0: none).
+struct MapState {
+    uint32_t hm;     // ballot of present high nibbles (bit 2h)
+    uint32_t sigma;  // codes incl. the zero row
+    uint32_t zrep;   // a byte absent from the map, replicated x4
+};
+
+// Builds the task's match masks (and, when needed, its byte -> code map) in
+// shared memory.  K is a runtime value and every loop over words / codes is
+// rolled: the build is one small piece of code shared by all lane shapes (it
+// runs once per task while the sweep code is hot, so its I-cache footprint
+// matters).
+//
+// Map reuse: tasks of one batch usually share their column alphabet (C2: the
+// same 20 letters), so the warp first builds the masks with the PREVIOUS
+// task's map and checks that every valid column matched one of its codes (the
+// OR of the masks equals the valid-column mask).  Only when some column is not
+// covered does it run the presence pass and the code scan and build again.
+// Codes of the old map absent from this task just get all-zero masks.
+//
 // Returns sigma (codes incl. the zero row) or 0 when the alphabet does not fit
 // the warp's shared-memory slice; *zrep receives a byte value absent from the
-// alphabet, replicated x4 (used to blank invalid rows in the sweep).
+// map, replicated x4 (used to blank invalid rows in the sweep).
 __device__ __forceinline__ uint32_t build_task(const BatchDev& d, const LanePair& p, int K, int s,
-                                            uint32_t sbase, uint32_t* zrep) {
+                                               uint32_t sbase, uint32_t* zrep, MapState& st) {
     const uint32_t lane = lane_id();
-    const uint32_t map = sbase;         // byte -> code
-    const uint32_t inv = sbase + 256u;  // u16 low-nibble presence per high nibble
+    const uint32_t map = sbase;           // byte -> code
+    const uint32_t inv = sbase + kInvOff;  // u16 low-nibble presence per high nibble
     const uint32_t pm = sbase + uint32_t(kMapBytes);
     const bool wide = pm_slotted(K);
     const uint32_t cs = wide ? 512u * uint32_t((K + 3) / 4) : 128u * pm_lane_words(K);
     const uint32_t ls = wide ? 16u : 4u * pm_lane_words(K);
-
-    // presence flags: one 32-bit word per byte value in the (not yet used) PM
-    // region -- lanes marking the same byte hit the same word (no conflict)
-    const uint32_t flags = pm;
-    __syncwarp();
-#pragma unroll
-    for (int i = 0; i < 2; ++i) sts_v4(flags + 16u * (lane * 2 + i), make_uint4(0u, 0u, 0u, 0u));
 
     // The lane's columns [c0, c0 + clen), read as the 16-byte aligned chunks
     // 0..2K of the region starting a_c bytes before them.
@@ -386,226 +396,193 @@ __device__ __forceinline__ uint32_t build_task(const BatchDev& d, const LanePair
         const uint32_t vm = i <= 2 * K ? valid_mask16(16 * i - a_c, clen) : 0u;
         return fetch_chunk(cstart, i, vm, p.col_lo, p.col_hi, d.safe16);
     };
-    // Stage the lane's 2K+1 column chunks in shared memory with cp.async
-    // (one exposed global latency per task instead of one per word and pass):
-    // at the end of the mask region, [chunk][lane] x 16 bytes.  Pass 2 reads
-    // the stage only when the task's masks do not reach it.
     const int nchk = 2 * K + 1;
     const uint32_t stage = pm + uint32_t(d.pm_bytes) - uint32_t(nchk) * 512u;
-    {
-        bool slow = false;
-        for (int i = 0; i < nchk; ++i) {
-            const uint8_t* src = cstart + 16 * i;
-            const uint32_t vm = valid_mask16(16 * i - a_c, clen);
-            const bool inb = src >= p.col_lo && src + 16 <= p.col_hi;
-            slow |= vm != 0u && !inb;
-            const void* g = (vm != 0u && inb) ? static_cast<const void*>(src)
-                                                : static_cast<const void*>(d.safe16);
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(stage + uint32_t(i) * 512u +
-                                                                           lane * 16u),
-                         "l"(g)
-                         : "memory");
-        }
-        asm volatile("cp.async.commit_group;\n\tcp.async.wait_all;" ::: "memory");
-        if (__any_sync(kFullMask, slow)) {  // a chunk straddles the buffer end (rare)
-            for (int i = 0; i < nchk; ++i) {
-                const uint8_t* src = cstart + 16 * i;
-                const uint32_t vm = valid_mask16(16 * i - a_c, clen);
-                if (vm != 0u && !(src >= p.col_lo && src + 16 <= p.col_hi))
-                    sts_v4(stage + uint32_t(i) * 512u + lane * 16u,
-                           load_chunk16(src, p.col_lo, p.col_hi));
-            }
-        }
-    }
     auto staged = [&](int i) {
         return i < nchk ? lds_v4(stage + uint32_t(i) * 512u + lane * 16u) : make_uint4(0u, 0u, 0u, 0u);
     };
-    __syncwarp();  // flags zeroed, stage filled
-
-    // pass 1: mark the bytes present
-    {
-        uint4 c0v = staged(0), c1v = staged(1), c2v = staged(2);
-#pragma unroll 1
-        for (int k = 0; k < K; ++k) {
-            const uint4 n1 = staged(2 * k + 3), n2 = staged(2 * k + 4);
-            uint32_t w[8];
-            word_bytes(c0v, c1v, c2v, q, fs, w);
-            const int nv = min(max(clen - 32 * k, 0), 32);
+    uint32_t sigma = st.sigma, hm = st.hm;
+    *zrep = st.zrep;
+    // attempt 0: the previous task's map; attempt 1: a fresh map
+    int attempt = (hm != 0u && sigma * cs <= uint32_t(d.pm_bytes)) ? 0 : 1;
+    for (;; ++attempt) {
+        bool use_stage = false;
+        if (attempt == 1) {
+            // presence flags: one 32-bit word per byte value in the (not yet
+            // used) PM region -- lanes marking the same byte hit the same word
+            const uint32_t flags = pm;
+            __syncwarp();
 #pragma unroll
-            for (int j = 0; j < 32; ++j)
-                if (j < nv) sts_u32(flags + 4u * __byte_perm(w[j >> 2], 0u, 0x4440u | uint32_t(j & 3)), 1u);
-            c0v = c2v;
-            c1v = n1;
-            c2v = n2;
-        }
-    }
-    __syncwarp();
-
-    // dense codes 1..sigma-1 in byte order (0 = no match), low-nibble
-    // presence per high nibble (in the inv region), zrep
-    uint32_t sigma, hm = 0;
-    uint32_t* hmask = &hm;
-    {
-        const uint4 f0 = lds_v4(flags + 32u * lane);
-        const uint4 f1 = lds_v4<16>(flags + 32u * lane);
-        const uint32_t present = (f0.x ? 1u : 0u) | (f0.y ? 2u : 0u) | (f0.z ? 4u : 0u) |
-                                 (f0.w ? 8u : 0u) | (f1.x ? 16u : 0u) | (f1.y ? 32u : 0u) |
-                                 (f1.z ? 64u : 0u) | (f1.w ? 128u : 0u);  // byte 8*lane + b
-        const uint32_t cnt = __popc(present);
-        uint32_t incl = cnt;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t v = __shfl_up_sync(kFullMask, incl, o);
-            if (int(lane) >= o) incl += v;
-        }
-        sigma = __shfl_sync(kFullMask, incl, 31) + 1;  // + the zero row
-        if (sigma > 256u || sigma * cs > uint32_t(d.pm_bytes)) return 0u;
-        uint32_t code = incl - cnt + 1;
-        uint32_t ox = 0, oy = 0;
-#pragma unroll
-        for (int b = 0; b < 8; ++b) {
-            if ((present >> b) & 1u) {
-                if (b < 4) ox |= code << (8 * b);
-                else oy |= code << (8 * (b - 4));
-                ++code;
+            for (int i = 0; i < 2; ++i) sts_v4(flags + 16u * (lane * 2 + i), make_uint4(0u, 0u, 0u, 0u));
+            // Stage the lane's 2K+1 column chunks in shared memory with cp.async
+            // (one exposed global latency per task instead of one per word and
+            // pass): at the end of the mask region, [chunk][lane] x 16 bytes.
+            bool slow = false;
+            for (int i = 0; i < nchk; ++i) {
+                const uint8_t* src = cstart + 16 * i;
+                const uint32_t vm = valid_mask16(16 * i - a_c, clen);
+                const bool inb = src >= p.col_lo && src + 16 <= p.col_hi;
+                slow |= vm != 0u && !inb;
+                const void* g = (vm != 0u && inb) ? static_cast<const void*>(src)
+                                                    : static_cast<const void*>(d.safe16);
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                                 stage + uint32_t(i) * 512u + lane * 16u),
+                             "l"(g)
+                             : "memory");
             }
-        }
-        // low-nibble presence per high nibble h (lanes 2h, 2h+1 hold bytes 16h..16h+15)
-        const uint32_t upper = __shfl_down_sync(kFullMask, present, 1);
-        const uint32_t nib16 = present | (upper << 8);
-        *hmask = __ballot_sync(kFullMask, (lane & 1u) == 0u && nib16 != 0u);
-        const uint32_t absent = ~present & 0xffu;  // exists: at most 255 bytes present
-        const uint32_t has = __ballot_sync(kFullMask, absent != 0u);
-        const uint32_t zb =
-            __shfl_sync(kFullMask, uint32_t(8 * lane) + __ffs(absent) - 1, __ffs(has) - 1);
-        *zrep = zb * 0x01010101u;
-        __syncwarp();
-        sts_v2(map + 8u * lane, ox, oy);
-        if ((lane & 1u) == 0u) sts_u16(inv + lane, nib16);
-    }
-    __syncwarp();
+            asm volatile("cp.async.commit_group;\n\tcp.async.wait_all;" ::: "memory");
+            if (__any_sync(kFullMask, slow)) {  // a chunk straddles the buffer end (rare)
+                for (int i = 0; i < nchk; ++i) {
+                    const uint8_t* src = cstart + 16 * i;
+                    const uint32_t vm = valid_mask16(16 * i - a_c, clen);
+                    if (vm != 0u && !(src >= p.col_lo && src + 16 <= p.col_hi))
+                        sts_v4(stage + uint32_t(i) * 512u + lane * 16u,
+                               load_chunk16(src, p.col_lo, p.col_hi));
+                }
+            }
+            __syncwarp();  // flags zeroed, stage filled
 
-    // pass 2, word by word: bit-planes, then every code's match mask
-    // = valid columns whose byte equals the code's byte value.
-    const uint32_t lane_off = wide ? lane * 16u : lane * ls;
-    const bool use_stage = sigma * cs <= uint32_t(d.pm_bytes) - uint32_t(nchk) * 512u;
-    auto chunk2 = [&](int i) { return use_stage ? staged(i) : chunk(i); };
-#if WLCS_BATCH_BUILD2
-    // two words per iteration: their bit-plane transposes are independent
-    // (twice the instruction-level parallelism of this latency-bound phase)
-    auto woff_of = [&](int k) {
-        return lane_off + (wide ? uint32_t((k >> 2) * 512 + (k & 3) * 4) : uint32_t(k * 4));
-    };
-    {
-        uint4 c0v = chunk2(0), c1v = chunk2(1), c2v = chunk2(2), c3v = chunk2(3), c4v = chunk2(4);
+            // pass 1: mark the bytes present
+            {
+                uint4 c0v = staged(0), c1v = staged(1), c2v = staged(2);
 #pragma unroll 1
-        for (int k = 0; k < K; k += 2) {
-            const uint4 n1 = chunk2(2 * k + 5), n2 = chunk2(2 * k + 6), n3 = chunk2(2 * k + 7),
-                        n4 = chunk2(2 * k + 8);
-            uint32_t w0[8], w1[8], P0[8], P1[8];
-            word_bytes(c0v, c1v, c2v, q, fs, w0);
-            word_bytes(c2v, c3v, c4v, q, fs, w1);
-            bit_planes8(w0, P0);
-            bit_planes8(w1, P1);
-            const bool has1 = k + 1 < K;  // warp-uniform
-            const int nv0 = min(max(clen - 32 * k, 0), 32);
-            const int nv1 = has1 ? min(max(clen - 32 * (k + 1), 0), 32) : 0;
-            const uint32_t vm0 = nv0 >= 32 ? 0xffffffffu : ((1u << nv0) - 1u);
-            const uint32_t vm1 = nv1 >= 32 ? 0xffffffffu : ((1u << nv1) - 1u);
-            uint32_t ca0 = pm + woff_of(k), ca1 = pm + woff_of(k + 1);
-            sts_u32(ca0, 0u);  // code 0: the zero row
-            if (has1) sts_u32(ca1, 0u);
-            const uint32_t a0[4] = {~(P0[0] | P0[1]), P0[0] & ~P0[1], ~P0[0] & P0[1], P0[0] & P0[1]};
-            const uint32_t b0[4] = {~(P0[2] | P0[3]), P0[2] & ~P0[3], ~P0[2] & P0[3], P0[2] & P0[3]};
-            const uint32_t a1[4] = {~(P1[0] | P1[1]), P1[0] & ~P1[1], ~P1[0] & P1[1], P1[0] & P1[1]};
-            const uint32_t b1[4] = {~(P1[2] | P1[3]), P1[2] & ~P1[3], ~P1[2] & P1[3], P1[2] & P1[3]};
-            uint32_t groups = hm;
-            while (groups) {  // warp-uniform
-                const uint32_t h = uint32_t(__ffs(groups) - 1) >> 1;
-                groups &= groups - 1u;
-                const uint32_t m4 = 0u - (h & 1u), m5 = 0u - ((h >> 1) & 1u),
-                               m6 = 0u - ((h >> 2) & 1u), m7 = 0u - ((h >> 3) & 1u);
-                const uint32_t hi0 = vm0 & ~((P0[4] ^ m4) | (P0[5] ^ m5) | (P0[6] ^ m6) | (P0[7] ^ m7));
-                const uint32_t hi1 = vm1 & ~((P1[4] ^ m4) | (P1[5] ^ m5) | (P1[6] ^ m6) | (P1[7] ^ m7));
-                const uint32_t nm = lds_u16(inv + 2u * h);
+                for (int k = 0; k < K; ++k) {
+                    const uint4 n1 = staged(2 * k + 3), n2 = staged(2 * k + 4);
+                    uint32_t w[8];
+                    word_bytes(c0v, c1v, c2v, q, fs, w);
+                    const int nv = min(max(clen - 32 * k, 0), 32);
 #pragma unroll
-                for (int jj = 0; jj < 4; ++jj) {
-                    if ((nm >> (4 * jj)) & 0xfu) {
-                        const uint32_t hb0 = hi0 & b0[jj], hb1 = hi1 & b1[jj];
+                    for (int j = 0; j < 32; ++j)
+                        if (j < nv)
+                            sts_u32(flags + 4u * __byte_perm(w[j >> 2], 0u, 0x4440u | uint32_t(j & 3)), 1u);
+                    c0v = c2v;
+                    c1v = n1;
+                    c2v = n2;
+                }
+            }
+            __syncwarp();
+
+            // dense codes 1..sigma-1 in byte order (0 = no match), low-nibble
+            // presence per high nibble (in the inv region), zrep
+            {
+                const uint4 f0 = lds_v4(flags + 32u * lane);
+                const uint4 f1 = lds_v4<16>(flags + 32u * lane);
+                const uint32_t present = (f0.x ? 1u : 0u) | (f0.y ? 2u : 0u) | (f0.z ? 4u : 0u) |
+                                         (f0.w ? 8u : 0u) | (f1.x ? 16u : 0u) | (f1.y ? 32u : 0u) |
+                                         (f1.z ? 64u : 0u) | (f1.w ? 128u : 0u);  // byte 8*lane + b
+                const uint32_t cnt = __popc(present);
+                uint32_t incl = cnt;
 #pragma unroll
-                        for (int ii = 0; ii < 4; ++ii) {
-                            if ((nm >> (4 * jj + ii)) & 1u) {
-                                ca0 += cs;
-                                ca1 += cs;
-                                sts_u32(ca0, hb0 & a0[ii]);
-                                if (has1) sts_u32(ca1, hb1 & a1[ii]);
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t v = __shfl_up_sync(kFullMask, incl, o);
+                    if (int(lane) >= o) incl += v;
+                }
+                sigma = __shfl_sync(kFullMask, incl, 31) + 1;  // + the zero row
+                st.hm = 0u;  // the map is about to change
+                if (sigma > 256u || sigma * cs > uint32_t(d.pm_bytes)) return 0u;
+                uint32_t code = incl - cnt + 1;
+                uint32_t ox = 0, oy = 0;
+#pragma unroll
+                for (int b = 0; b < 8; ++b) {
+                    if ((present >> b) & 1u) {
+                        if (b < 4) ox |= code << (8 * b);
+                        else oy |= code << (8 * (b - 4));
+                        ++code;
+                    }
+                }
+                // low-nibble presence per high nibble h (lanes 2h, 2h+1 hold bytes 16h..16h+15)
+                const uint32_t upper = __shfl_down_sync(kFullMask, present, 1);
+                const uint32_t nib16 = present | (upper << 8);
+                hm = __ballot_sync(kFullMask, (lane & 1u) == 0u && nib16 != 0u);
+                const uint32_t absent = ~present & 0xffu;  // exists: at most 255 bytes present
+                const uint32_t has = __ballot_sync(kFullMask, absent != 0u);
+                const uint32_t zb =
+                    __shfl_sync(kFullMask, uint32_t(8 * lane) + __ffs(absent) - 1, __ffs(has) - 1);
+                *zrep = zb * 0x01010101u;
+                __syncwarp();
+                sts_v2(map + 8u * lane, ox, oy);
+                if ((lane & 1u) == 0u) sts_u16(inv + lane, nib16);
+            }
+            __syncwarp();
+            use_stage = sigma * cs <= uint32_t(d.pm_bytes) - uint32_t(nchk) * 512u;
+        }
+
+        // pass 2, two words per iteration (their bit-plane transposes are
+        // independent): bit-planes, then every code's match mask = valid
+        // columns whose byte equals the code's byte value; `covered` checks
+        // that every valid column matched a code of the map
+        const uint32_t lane_off = wide ? lane * 16u : lane * ls;
+        auto chunk2 = [&](int i) { return use_stage ? staged(i) : chunk(i); };
+        auto woff_of = [&](int k) {
+            return lane_off + (wide ? uint32_t((k >> 2) * 512 + (k & 3) * 4) : uint32_t(k * 4));
+        };
+        bool covered = true;
+        {
+            uint4 c0v = chunk2(0), c1v = chunk2(1), c2v = chunk2(2), c3v = chunk2(3), c4v = chunk2(4);
+#pragma unroll 1
+            for (int k = 0; k < K; k += 2) {
+                const uint4 n1 = chunk2(2 * k + 5), n2 = chunk2(2 * k + 6), n3 = chunk2(2 * k + 7),
+                            n4 = chunk2(2 * k + 8);
+                uint32_t w0[8], w1[8], P0[8], P1[8];
+                word_bytes(c0v, c1v, c2v, q, fs, w0);
+                word_bytes(c2v, c3v, c4v, q, fs, w1);
+                bit_planes8(w0, P0);
+                bit_planes8(w1, P1);
+                const bool has1 = k + 1 < K;  // warp-uniform
+                const int nv0 = min(max(clen - 32 * k, 0), 32);
+                const int nv1 = has1 ? min(max(clen - 32 * (k + 1), 0), 32) : 0;
+                const uint32_t vm0 = nv0 >= 32 ? 0xffffffffu : ((1u << nv0) - 1u);
+                const uint32_t vm1 = nv1 >= 32 ? 0xffffffffu : ((1u << nv1) - 1u);
+                uint32_t ca0 = pm + woff_of(k), ca1 = pm + woff_of(k + 1);
+                sts_u32(ca0, 0u);  // code 0: the zero row
+                if (has1) sts_u32(ca1, 0u);
+                const uint32_t a0[4] = {~(P0[0] | P0[1]), P0[0] & ~P0[1], ~P0[0] & P0[1], P0[0] & P0[1]};
+                const uint32_t b0[4] = {~(P0[2] | P0[3]), P0[2] & ~P0[3], ~P0[2] & P0[3], P0[2] & P0[3]};
+                const uint32_t a1[4] = {~(P1[0] | P1[1]), P1[0] & ~P1[1], ~P1[0] & P1[1], P1[0] & P1[1]};
+                const uint32_t b1[4] = {~(P1[2] | P1[3]), P1[2] & ~P1[3], ~P1[2] & P1[3], P1[2] & P1[3]};
+                uint32_t cov0 = 0, cov1 = 0;
+                uint32_t groups = hm;
+                while (groups) {  // warp-uniform
+                    const uint32_t h = uint32_t(__ffs(groups) - 1) >> 1;
+                    groups &= groups - 1u;
+                    const uint32_t m4 = 0u - (h & 1u), m5 = 0u - ((h >> 1) & 1u),
+                                   m6 = 0u - ((h >> 2) & 1u), m7 = 0u - ((h >> 3) & 1u);
+                    const uint32_t hi0 = vm0 & ~((P0[4] ^ m4) | (P0[5] ^ m5) | (P0[6] ^ m6) | (P0[7] ^ m7));
+                    const uint32_t hi1 = vm1 & ~((P1[4] ^ m4) | (P1[5] ^ m5) | (P1[6] ^ m6) | (P1[7] ^ m7));
+                    const uint32_t nm = lds_u16(inv + 2u * h);
+#pragma unroll
+                    for (int jj = 0; jj < 4; ++jj) {
+                        if ((nm >> (4 * jj)) & 0xfu) {
+                            const uint32_t hb0 = hi0 & b0[jj], hb1 = hi1 & b1[jj];
+#pragma unroll
+                            for (int ii = 0; ii < 4; ++ii) {
+                                if ((nm >> (4 * jj + ii)) & 1u) {
+                                    ca0 += cs;
+                                    ca1 += cs;
+                                    const uint32_t mk0 = hb0 & a0[ii], mk1 = hb1 & a1[ii];
+                                    cov0 |= mk0;
+                                    cov1 |= mk1;
+                                    sts_u32(ca0, mk0);
+                                    if (has1) sts_u32(ca1, mk1);
+                                }
                             }
                         }
                     }
                 }
+                covered = covered && cov0 == vm0 && cov1 == vm1;
+                c0v = c4v;
+                c1v = n1;
+                c2v = n2;
+                c3v = n3;
+                c4v = n4;
             }
-            c0v = c4v;
-            c1v = n1;
-            c2v = n2;
-            c3v = n3;
-            c4v = n4;
         }
+        if (attempt == 1 || __all_sync(kFullMask, covered)) break;
     }
-#else
-    {
-        uint4 c0v = chunk2(0), c1v = chunk2(1), c2v = chunk2(2);
-#pragma unroll 1
-        for (int k = 0; k < K; ++k) {
-            const uint4 n1 = chunk2(2 * k + 3), n2 = chunk2(2 * k + 4);
-            uint32_t w[8], P[8];
-            word_bytes(c0v, c1v, c2v, q, fs, w);
-            bit_planes8(w, P);
-            const int nv = min(max(clen - 32 * k, 0), 32);
-            const uint32_t vmask = nv >= 32 ? 0xffffffffu : ((1u << nv) - 1u);
-            const uint32_t woff =
-                lane_off + (wide ? uint32_t((k >> 2) * 512 + (k & 3) * 4) : uint32_t(k * 4));
-            sts_u32(pm + woff, 0u);  // code 0: the zero row
-            // codes are dense in byte order and the walk below visits the
-            // present bytes in increasing order: code c's row is one stride on
-            uint32_t caddr = pm + woff;
-            // match mask of byte v = h*16 + 4j + i:
-            //   hi(h) & b[j] & a[i],  a[i] / b[j] = equality masks of the bit
-            //   pairs (planes 0,1) / (planes 2,3), hi(h) = planes 4..7 == h
-            const uint32_t a[4] = {~(P[0] | P[1]), P[0] & ~P[1], ~P[0] & P[1], P[0] & P[1]};
-            const uint32_t b[4] = {~(P[2] | P[3]), P[2] & ~P[3], ~P[2] & P[3], P[2] & P[3]};
-            uint32_t groups = hm;
-            while (groups) {  // warp-uniform
-                const uint32_t h = uint32_t(__ffs(groups) - 1) >> 1;
-                groups &= groups - 1u;
-                const uint32_t hi_acc =
-                    vmask & ~((P[4] ^ (0u - (h & 1u))) | (P[5] ^ (0u - ((h >> 1) & 1u))) |
-                              (P[6] ^ (0u - ((h >> 2) & 1u))) | (P[7] ^ (0u - ((h >> 3) & 1u))));
-                const uint32_t nm = lds_u16(inv + 2u * h);
-#pragma unroll
-                for (int jj = 0; jj < 4; ++jj) {
-                    if ((nm >> (4 * jj)) & 0xfu) {
-                        const uint32_t hb = hi_acc & b[jj];
-#pragma unroll
-                        for (int ii = 0; ii < 4; ++ii) {
-                            if ((nm >> (4 * jj + ii)) & 1u) {
-                                caddr += cs;
-                                sts_u32(caddr, hb & a[ii]);
-                            }
-                        }
-                    }
-                }
-            }
-            c0v = c2v;
-            c1v = n1;
-            c2v = n2;
-        }
-    }
-#endif
     __syncwarp();
-    // the inverse table is done: zero it for the sweep (the all-zero map of
-    // chunks outside a row string)
-    sts_v2(inv + 8u * lane, 0u, 0u);
-    __syncwarp();
+    st.hm = hm;
+    st.sigma = sigma;
+    st.zrep = *zrep;
     return sigma;
 }
 
@@ -675,7 +652,7 @@ __device__ __forceinline__ int sweep_task(const BatchDev& d, const LanePair& p, 
     if (!__all_sync(kFullMask, inb)) return sweep_task_generic<CHAIN, K>(d, p, S, s, smem, zrep);
     const uint32_t lane = lane_id();
     const uint32_t map_a = sbase;
-    const uint32_t zmap_a = map_a + 256u;  // zeroed after the build: every byte -> code 0
+    const uint32_t zmap_a = map_a + kZmapOff;  // all zero: every byte -> code 0
     const uint32_t pm_a = map_a + uint32_t(kMapBytes) + PmLayout<K>::word_offset(lane, 0);
     uint32_t V[K];
 #pragma unroll
@@ -739,6 +716,8 @@ __global__ void __launch_bounds__(32) batch_main_kernel(BatchDev d) {
     // from SR_CgaCtaId inside the loops)
     uint32_t sbase;
     asm volatile("mov.b32 %0, %1;" : "=r"(sbase) : "r"(smem_u32(smem)));
+    sts_v2(sbase + kZmapOff + 8u * lane, 0u, 0u);  // the all-zero map, once
+    MapState mstate{0u, 0u, 0u};                    // no map yet
     for (;;) {
         uint32_t t = 0;
         if (lane == 0) t = atomicAdd(d.meta + kMetaCounter, 1u);
@@ -757,7 +736,7 @@ __global__ void __launch_bounds__(32) batch_main_kernel(BatchDev d) {
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(trb0));
 #endif
         uint32_t zrep = 0;
-        if (build_task(d, p, K, s, sbase, &zrep) == 0u) {
+        if (build_task(d, p, K, s, sbase, &zrep, mstate) == 0u) {
             // Alphabet too large for this warp's shared-memory slice.
             if (active && s == 0) d.overflow[atomicAdd(d.meta + kMetaOverflow, 1u)] = pair;
             continue;
