@@ -18,6 +18,18 @@ namespace wlcs {
 constexpr unsigned kFullMask = 0xffffffffu;
 constexpr int kRowsPerStep = 16;  // one 16-byte chunk of the row string per step
 
+// 16-byte read-only load that also asks L2 to fetch the surrounding 256-byte
+// block (ld.global.nc.L2::256B): a lane streaming its own string one chunk
+// per step gets the next 15 chunks staged in L2 by the first miss, so the
+// one-step-ahead register prefetch then hits L2 instead of HBM.
+__device__ __forceinline__ uint4 ldg_l2pf(const uint4* p) {
+    uint4 v;
+    asm("ld.global.nc.L2::256B.v4.u32 {%0, %1, %2, %3}, [%4];"
+        : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+        : "l"(p));
+    return v;
+}
+
 // Byte-wise gather of a chunk that straddles the allocation end (rare; kept
 // out of line so the callers' hot loops stay small).
 static __device__ __noinline__ uint4 load_chunk16_slow(const uint8_t* p, const uint8_t* alloc_lo,
@@ -85,7 +97,7 @@ __device__ __forceinline__ uint4 fetch_chunk_fast(const uint8_t* p, uint32_t vm,
     const bool inb = p >= alloc_lo && p + 16 <= alloc_hi;
     slow = vm != 0u && !inb;
     const uint4* src = (vm != 0u && inb) ? reinterpret_cast<const uint4*>(p) : safe;
-    return __ldg(src);
+    return ldg_l2pf(src);
 }
 
 __device__ __forceinline__ int warp_max(int v) {
