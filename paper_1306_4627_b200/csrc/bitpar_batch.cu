@@ -670,7 +670,7 @@ __device__ __forceinline__ int sweep_task(const BatchDev& d, const LanePair& p, 
     for (int t = 0; t < T; ++t) {
         const int ch = t - s;
         const bool nv = unsigned(ch + 1) < unsigned(nrch);
-        const uint4 nxt = __ldg(nv ? nptr : d.safe16);
+        const uint4 nxt = ldg_l2pf(nv ? nptr : d.safe16);
         ++nptr;
         uint32_t cin = 0;
         if constexpr (CHAIN) {
