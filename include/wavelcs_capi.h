@@ -89,6 +89,18 @@ int wlcs_length_ex(const uint8_t* x, size_t m, const uint8_t* y, size_t n, size_
 int wlcs_subsequence(const uint8_t* x, size_t m, const uint8_t* y, size_t n,
                      size_t memory_budget, uint8_t* out, size_t cap, size_t* out_len);
 
+/* Same, with a cap on the traceback's device memory (stored bit rows plus
+ * checkpoints), row_cap bytes; 0 = automatic (half the free device memory, at
+ * most 8 GiB).  Within the cap the fill stores every row (M * N / 8 bytes);
+ * beyond it the traceback runs in row bands: a first fill keeps the bit
+ * vector of every B-th row, then each band is filled again from its
+ * checkpoint and walked, bottom band first -- the same rows and rule, hence
+ * the same string, in O(N (M / B + B)) bits.  WLCS_E_OUT_OF_MEMORY when even
+ * one 256-row band does not fit row_cap. */
+int wlcs_subsequence_ex(const uint8_t* x, size_t m, const uint8_t* y, size_t n,
+                        size_t memory_budget, size_t row_cap, uint8_t* out, size_t cap,
+                        size_t* out_len);
+
 /* Batch of independent pairs (new; the reference loops one pair at a time,
  * src/bench.cpp:77-129).  Pair k is x = xs[x_off[k] .. x_off[k+1]) and
  * y = ys[y_off[k] .. y_off[k+1]); offsets are absolute, non-decreasing,

@@ -99,6 +99,7 @@ lib.wlcs_device_count.restype = ctypes.c_int
 lib.wlcs_check_capacity.argtypes = [_sz, _sz, _sz]
 lib.wlcs_length_ex.argtypes = [_vp, _sz, _vp, _sz, _sz, ctypes.c_int, _u32p]
 lib.wlcs_subsequence.argtypes = [_vp, _sz, _vp, _sz, _sz, _vp, _sz, ctypes.POINTER(_sz)]
+lib.wlcs_subsequence_ex.argtypes = [_vp, _sz, _vp, _sz, _sz, _sz, _vp, _sz, ctypes.POINTER(_sz)]
 lib.wlcs_length_batch_ex.argtypes = [_vp, _u64p, _vp, _u64p, _sz, ctypes.c_int, _u32p]
 lib.wlcs_length_batch_device.argtypes = [_vp, _vp, _vp, _vp, _sz, ctypes.c_uint64,
                                          ctypes.c_uint64, ctypes.c_int, _vp, _vp]
@@ -162,14 +163,16 @@ def lcs_length(x, y, memory_budget: int = DEFAULT_MEMORY_BUDGET,
     return int(out.value)
 
 
-def lcs_subsequence(x, y, memory_budget: int = DEFAULT_MEMORY_BUDGET) -> bytes:
-    """traceback(lcs_fill_parallel(x, y).back, x, M, N) as one call (serial.hpp:30)."""
+def lcs_subsequence(x, y, memory_budget: int = DEFAULT_MEMORY_BUDGET, row_cap: int = 0) -> bytes:
+    """traceback(lcs_fill_parallel(x, y).back, x, M, N) as one call (serial.hpp:30).
+    row_cap bounds the traceback's device memory (0 = automatic); beyond it
+    the traceback runs in row bands recomputed from checkpoints."""
     xb, yb = _as_bytes(x), _as_bytes(y)
     cap = max(1, min(len(xb), len(yb)))
     out = ctypes.create_string_buffer(cap)
     n = _sz()
-    _check(lib.wlcs_subsequence(xb, len(xb), yb, len(yb), memory_budget, out, cap,
-                                ctypes.byref(n)))
+    _check(lib.wlcs_subsequence_ex(xb, len(xb), yb, len(yb), memory_budget, row_cap, out, cap,
+                                   ctypes.byref(n)))
     return out.raw[: n.value]
 
 

@@ -242,7 +242,8 @@ __global__ void __launch_bounds__(32, 1) pair_strip_kernel(PairDev d) {
         const int64_t plane = P.plane;
         uint32_t V[K];
 #pragma unroll
-        for (int k = 0; k < K; ++k) V[k] = 0xffffffffu;
+        for (int k = 0; k < K; ++k)
+            V[k] = (P.v_in && g * K + k < P.W) ? __ldg(P.v_in + g * K + k) : 0xffffffffu;
         // the slice's first strip takes its carries from ext_in and its last
         // strip sends them to ext_out when the pair is split across GPUs
         const bool ext_left = strip == 0 && P.ext_in != nullptr;
@@ -357,6 +358,13 @@ __global__ void __launch_bounds__(32, 1) pair_strip_kernel(PairDev d) {
                 }
                 cin_lo = nl << 24;
                 cin_hi = nh << 24;
+                if (P.ckpt_out && valid && (ch + 1) % P.ckpt_chunks == 0 && ch + 1 < nchunks) {
+                    // checkpoint (ch + 1) / ckpt_chunks: V after the chunk's rows
+                    uint32_t* c = P.ckpt_out + int64_t((ch + 1) / P.ckpt_chunks - 1) * P.W;
+#pragma unroll
+                    for (int k = 0; k < K; ++k)
+                        if (g * K + k < P.W) c[g * K + k] = V[k];
+                }
             }
         }
         __syncwarp();
@@ -560,7 +568,7 @@ __global__ void __launch_bounds__(kWalkCand) walk_spec_kernel(PairDev d, int32_t
     for (int64_t i = top - threadIdx.x; i > lo; i -= blockDim.x)
         codes[top - i] = walk_code<K>(P, i - 1);
     __syncthreads();
-    int64_t j = walk_cand(walk_guess(top, M, N), int(threadIdx.x), N);
+    int64_t j = walk_cand(walk_guess(P.walk_row0 + top, P.walk_mtot, N), int(threadIdx.x), N);
     int32_t* ck = ckpt + k * (kWalkNCkpt * kWalkCand) + threadIdx.x;
     for (int64_t i = top; i > lo; --i) {
         uint32_t dg;
@@ -581,7 +589,7 @@ __global__ void __launch_bounds__(32) walk_resolve_kernel(PairDev d, const int32
     const int64_t M = P.rows, N = P.cols;
     const int64_t nb = (M + kWalkRows - 1) / kWalkRows;
     const int lane = int(lane_id());
-    int64_t j = N;
+    int64_t j = P.walk_entry ? int64_t(*P.walk_entry) : N;
     uint32_t miss = 0;
     const long long t_start = clock64();
     long long t_miss = 0;
@@ -593,7 +601,8 @@ __global__ void __launch_bounds__(32) walk_resolve_kernel(PairDev d, const int32
     __shared__ int64_t gs[2][kGroup];  // the blocks' diagonal guesses
     auto stage = [&](int64_t grp) {
         const int64_t k0 = grp * kGroup;
-        if (k0 + lane < nb) gs[grp & 1][lane] = walk_guess(M - (k0 + lane) * kWalkRows, M, N);
+        if (k0 + lane < nb)
+            gs[grp & 1][lane] = walk_guess(P.walk_row0 + M - (k0 + lane) * kWalkRows, P.walk_mtot, N);
         if (k0 < nb) {
             const int64_t n16 = ((nb - k0 < kGroup ? nb - k0 : kGroup) * kWalkCand) / 4;
             const int4* src = reinterpret_cast<const int4*>(exits + k0 * kWalkCand);
@@ -683,6 +692,7 @@ __global__ void __launch_bounds__(32) walk_resolve_kernel(PairDev d, const int32
         }
     }
     if (lane == 0) {
+        if (P.walk_entry) *P.walk_entry = int32_t(j);  // the next band up enters here
         misses[0] = miss;
         misses[1] = uint32_t(t_miss >> 10);                    // diagnostics: kilocycles in
         misses[2] = uint32_t((clock64() - t_start) >> 10);     // fallback walks / in total
@@ -714,20 +724,30 @@ __global__ void __launch_bounds__(32 * kWalkWarps) walk_emit_kernel(PairDev d, c
 
 // 4a. one thread: output offsets (forward order = blocks from the top rows)
 __global__ void walk_scan_kernel(const uint32_t* counts, int64_t nb, uint32_t* offsets,
-                                 unsigned long long* total) {
+                                 unsigned long long* total, unsigned long long* place,
+                                 unsigned long long* base) {
     unsigned long long run = 0;
     for (int64_t k = nb - 1; k >= 0; --k) {
         offsets[k] = uint32_t(run);
         run += counts[k];
     }
     *total = run;
+    // banded traceback: this band's bytes end where the lower bands' begin
+    unsigned long long b = 0;
+    if (place) {
+        b = place[0] - place[1] - run;
+        place[1] += run;
+    }
+    *base = b;
 }
 
 // 4b. one warp per block writes its emitted bytes in row order: lane t
 // takes 8 consecutive rows, a warp scan gives its output position
 __global__ void __launch_bounds__(128) walk_write_kernel(const uint8_t* x, int64_t M,
                                                          const uint8_t* flags,
-                                                         const uint32_t* offsets, uint8_t* out) {
+                                                         const uint32_t* offsets,
+                                                         const unsigned long long* base,
+                                                         uint8_t* out) {
     static_assert(kWalkRows == 256, "8 rows per lane");
     const int64_t nb = (M + kWalkRows - 1) / kWalkRows;
     const int64_t k = int64_t(blockIdx.x) * 4 + (threadIdx.x >> 5);
@@ -749,7 +769,7 @@ __global__ void __launch_bounds__(128) walk_write_kernel(const uint8_t* x, int64
         const uint32_t t = __shfl_up_sync(kFullMask, incl, o);
         if (lane >= o) incl += t;
     }
-    uint8_t* o = out + offsets[k] + (incl - n);
+    uint8_t* o = out + *base + offsets[k] + (incl - n);
 #pragma unroll
     for (int r = 0; r < 8; ++r)
         if ((f >> r) & 1u) *o++ = x[q0 + r];
@@ -990,7 +1010,7 @@ cudaError_t pair_fill(const PairDev& d, int K, bool store, int sms, cudaStream_t
 
 size_t pair_walk_scratch_bytes(int64_t rows) {
     const int64_t nb = (rows + kWalkRows - 1) / kWalkRows;
-    return size_t(nb) * kWalkCand * 4 * (1 + kWalkNCkpt) + size_t(nb) * 12 + size_t(rows) + 64;
+    return size_t(nb) * kWalkCand * 4 * (1 + kWalkNCkpt) + size_t(nb) * 12 + size_t(rows) + 128;
 }
 
 cudaError_t pair_walk(const PairDev& d, int K, const uint8_t* x, uint8_t* out,
@@ -1003,7 +1023,9 @@ cudaError_t pair_walk(const PairDev& d, int K, const uint8_t* x, uint8_t* out,
     int32_t* entry = ckpt + nb * kWalkCand * kWalkNCkpt;
     uint32_t* counts = reinterpret_cast<uint32_t*>(entry + nb);
     uint32_t* offsets = counts + nb;
-    uint8_t* flags = reinterpret_cast<uint8_t*>(offsets + nb);
+    unsigned long long* base = reinterpret_cast<unsigned long long*>(
+        (reinterpret_cast<uintptr_t>(offsets + nb) + 15) & ~uintptr_t(15));
+    uint8_t* flags = reinterpret_cast<uint8_t*>(base + 2);
     const int emit_ctas = int((nb + kWalkWarps - 1) / kWalkWarps);
     cudaError_t e = cudaMemsetAsync(flags, 0, size_t(M), stream);
     if (e != cudaSuccess) return e;
@@ -1019,8 +1041,9 @@ cudaError_t pair_walk(const PairDev& d, int K, const uint8_t* x, uint8_t* out,
         mark(2);
         emit<<<emit_ctas, 32 * kWalkWarps, 0, stream>>>(d, entry, flags, counts);
         mark(3);
-        walk_scan_kernel<<<1, 1, 0, stream>>>(counts, nb, offsets, out_len);
-        walk_write_kernel<<<emit_ctas, 128, 0, stream>>>(x, M, flags, offsets, out);
+        walk_scan_kernel<<<1, 1, 0, stream>>>(counts, nb, offsets, out_len,
+                                              d.prob[0].walk_place, base);
+        walk_write_kernel<<<emit_ctas, 128, 0, stream>>>(x, M, flags, offsets, base, out);
         mark(4);
         if (dbg) {
             cudaEventSynchronize(ev[4]);

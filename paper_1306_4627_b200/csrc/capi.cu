@@ -95,6 +95,7 @@ struct Ctx {
     DevBuf xs, ys, xoff, yoff, out, ws, ws2, wcarry;
     // single pair
     DevBuf px, py, pmg, carry, small, rows, outrev, codes, ry, vbuf, wave, sink, walk, tile;
+    DevBuf ckpt, bandcodes;  // banded traceback
     ~Ctx() {
         if (hscratch) cudaFreeHost(hscratch);
         for (cudaEvent_t e : chunk_ev) cudaEventDestroy(e);
@@ -263,6 +264,9 @@ void set_problem(wlcs::FillProblem& P, int64_t rows, uint32_t* pmg, int64_t cols
     P.Mpad = int64_t(P.nchunks) * 16;
     P.Dpad = P.Mpad + 512;
     P.cwords = ((int64_t(P.nchunks) + 3) & ~int64_t(3)) + 16;
+    P.walk_row0 = 0;
+    P.walk_mtot = rows;
+    P.ckpt_chunks = 1;
 }
 
 bool use_split(int64_t rows, bool store) {
@@ -295,9 +299,9 @@ int watchdog_failed(Ctx& c) {
 }
 
 int pair_setup(Ctx& c, const uint8_t* d_row, int64_t rows, const uint8_t* d_col, int64_t cols,
-               bool store, PairPlan& plan) {
+               bool store, PairPlan& plan, bool allow_split = true) {
     wlcs::PairDev& d = plan.d;
-    const bool split = use_split(rows, store);
+    const bool split = allow_split && use_split(rows, store);
     d.nprob = split ? 2 : 1;
     d.colp0 = d_col;
     d.prob[0].cols = cols;
@@ -823,6 +827,169 @@ extern "C" int wlcs_colsplit_emulate(const uint8_t* x, size_t m, const uint8_t* 
 }
 
 namespace {
+// ---- recovered subsequence ------------------------------------------------
+// Two ways to the same bytes (the reference's traceback, serial.cpp:36-61,
+// with the LEFT rule of cell.hpp:30-38):
+//  * full:   one fill that stores every row's bit vector (M * N / 8 bytes),
+//            then the parallel walk (bitpar_pair.cu pair_walk);
+//  * banded: bounded memory -- a first fill keeps only every B-th row's bit
+//            vector (checkpoints, (M / B) * N / 8 bytes); then, from the
+//            bottom band up, each band of B rows is filled again from its
+//            checkpoint with its rows stored (B * N / 8 bytes) and walked from
+//            the column where the band below was left.  Same rows, same walk
+//            rule, hence the same string; memory O(N (M / B + B)) instead of
+//            O(M N), for about twice the fill work.
+// The band size comes from `row_cap` (bytes of stored bit rows +
+// checkpoints); row_cap = 0 picks the full path while it fits an automatic
+// cap (half the free device memory, at most 8 GiB) and bands beyond it.
+
+// bytes of stored bit rows for `rows` rows of problem P at K words per lane
+size_t store_bytes(const wlcs::FillProblem& P, int K, int64_t rows) {
+    const int64_t mpad = (rows + 15) / 16 * 16;
+    return size_t(P.nstrips) * 32 * size_t(mpad + 512) * size_t(K) * 4;
+}
+
+// band rows B (a multiple of the walk's 256-row blocks) so that the stored
+// band plus the checkpoints fit `cap`; 0 when even 256 rows do not fit
+int64_t band_rows_for(const wlcs::FillProblem& P, int K, int64_t M, size_t cap) {
+    for (int64_t B = ((M + 255) / 256) * 256; B >= 256; B -= (B > 4096 ? B / 8 / 256 * 256 : 256)) {
+        const int64_t nb = (M + B - 1) / B;
+        const size_t need = store_bytes(P, K, B) + size_t(nb - 1) * size_t(P.W) * 4;
+        if (need <= cap) return B;
+        if (B <= 4096 && B - 256 < 256) break;
+    }
+    return 0;
+}
+
+int subsequence_banded(Ctx& c, const uint8_t* dx, size_t m, const uint8_t* dy, size_t n,
+                       size_t cap, unsigned long long* len_out) {
+    PairPlan plan;
+    int rc = pair_setup(c, dx, int64_t(m), dy, int64_t(n), false, plan, /*allow_split=*/false);
+    if (rc) return rc;
+    wlcs::PairDev& d = plan.d;
+    const int K = plan.K;
+    const wlcs::FillProblem full = d.prob[0];
+    const int64_t M = full.rows, W = full.W;
+    const int64_t B = band_rows_for(full, K, M, cap);
+    if (B == 0)
+        return fail(WLCS_E_OUT_OF_MEMORY,
+                    "traceback memory cap of " + std::to_string(cap) +
+                        " bytes is below one 256-row band (" +
+                        std::to_string(store_bytes(full, K, 256)) + " bytes)");
+    const int64_t nbands = (M + B - 1) / B;
+    // pass 1: the whole fill, keeping V after every B rows (and the length)
+    WLCS_CUDA(c.ckpt.ensure(size_t(std::max<int64_t>(nbands - 1, 1)) * size_t(W) * 4));
+    d.prob[0].ckpt_out = c.ckpt.as<uint32_t>();
+    d.prob[0].ckpt_chunks = int(B / 16);
+    if (c.timing && !c.ev0) {
+        WLCS_CUDA(cudaEventCreate(&c.ev0));
+        WLCS_CUDA(cudaEventCreate(&c.ev1));
+    }
+    if (c.timing) WLCS_CUDA(cudaEventRecord(c.ev0, c.stream));
+    WLCS_CUDA(wlcs::pair_fill(d, K, false, c.sms, c.stream));
+    // the walk's state between bands: entry column, {L, bytes emitted}
+    uint8_t* sb = c.small.as<uint8_t>();
+    unsigned long long* zeros_dev = pair_zeros_ptr(c);
+    int32_t* d_entry = reinterpret_cast<int32_t*>(sb + 1704);
+    unsigned long long* d_place = reinterpret_cast<unsigned long long*>(sb + 1712);
+    int32_t* h_entry = reinterpret_cast<int32_t*>(c.hscratch + 8);
+    *h_entry = int32_t(n);
+    WLCS_CUDA(cudaMemcpyAsync(d_entry, h_entry, 4, cudaMemcpyHostToDevice, c.stream));
+    WLCS_CUDA(cudaMemcpyAsync(d_place, zeros_dev, 8, cudaMemcpyDeviceToDevice, c.stream));
+    WLCS_CUDA(cudaMemsetAsync(d_place + 1, 0, 8, c.stream));
+    // band buffers
+    WLCS_CUDA(c.rows.ensure(store_bytes(full, K, B)));
+    WLCS_CUDA(c.bandcodes.ensure(4 * size_t(wlcs::pair_code_plane(int(B / 16))) * 16));
+    WLCS_CUDA(c.walk.ensure(wlcs::pair_walk_scratch_bytes(B)));
+    const size_t maxlen = std::min(m, n);
+    WLCS_CUDA(c.outrev.ensure(maxlen + 16));
+    unsigned long long* dlen = zeros_dev + 1;
+    uint32_t* dmiss = reinterpret_cast<uint32_t*>(zeros_dev + 2);
+    for (int64_t b = nbands - 1; b >= 0; --b) {
+        const int64_t r0 = b * B, rb = std::min<int64_t>(B, M - r0);
+        wlcs::FillProblem Pb = full;
+        set_problem(Pb, rb, const_cast<uint32_t*>(full.pmg), full.cols, K);
+        Pb.carry = c.carry.as<uint32_t>();
+        Pb.v_in = b > 0 ? c.ckpt.as<uint32_t>() + (b - 1) * W : nullptr;
+        Pb.ckpt_out = nullptr;
+        Pb.zeros = nullptr;
+        Pb.v_out = nullptr;
+        Pb.rows_out = c.rows.as<uint32_t>();
+        Pb.walk_row0 = r0;
+        Pb.walk_mtot = M;
+        Pb.walk_entry = d_entry;
+        Pb.walk_place = d_place;
+        WLCS_CUDA(wlcs::pair_code_rows(dx + r0, rb, false, d.map, K, Pb, c.bandcodes.as<uint4>(),
+                                       c.stream));
+        WLCS_CUDA(cudaMemsetAsync(Pb.carry, 0, size_t(Pb.nstrips) * size_t(Pb.cwords) * 4,
+                                  c.stream));
+        WLCS_CUDA(cudaMemsetAsync(d.ticket, 0, 4 * wlcs::kMaxProblems, c.stream));
+        wlcs::PairDev db = d;
+        db.nprob = 1;
+        db.prob[0] = Pb;
+        WLCS_CUDA(wlcs::pair_fill(db, K, true, c.sms, c.stream));
+        WLCS_CUDA(wlcs::pair_walk(db, K, dx + r0, c.outrev.as<uint8_t>(), dlen, c.walk.p, dmiss,
+                                  c.stream));
+    }
+    if (c.timing) WLCS_CUDA(cudaEventRecord(c.ev1, c.stream));
+    WLCS_CUDA(cudaMemcpyAsync(c.hscratch, d_place, 16, cudaMemcpyDeviceToHost, c.stream));
+    WLCS_CUDA(stream_wait(c.stream));
+    if (c.timing) {
+        WLCS_CUDA(cudaEventElapsedTime(&c.last_main_ms, c.ev0, c.ev1));
+        c.timing_pending = false;
+    }
+    if (c.hscratch[1] != c.hscratch[0])
+        return fail(WLCS_E_INTERNAL, "banded traceback emitted " + std::to_string(c.hscratch[1]) +
+                                         " bytes for an LCS of length " +
+                                         std::to_string(c.hscratch[0]));
+    *len_out = c.hscratch[0];
+    return WLCS_OK;
+}
+
+int subsequence_full(Ctx& c, const uint8_t* dx, size_t m, const uint8_t* dy, size_t n,
+                     unsigned long long* len_out) {
+    // Orientation matters for tie-breaking: rows = x (parent), columns = y.
+    PairPlan plan;
+    int rc = pair_setup(c, dx, int64_t(m), dy, int64_t(n), true, plan);
+    if (rc) return rc;
+    if (c.timing && !c.ev0) {
+        WLCS_CUDA(cudaEventCreate(&c.ev0));
+        WLCS_CUDA(cudaEventCreate(&c.ev1));
+    }
+    if (c.timing) WLCS_CUDA(cudaEventRecord(c.ev0, c.stream));
+    WLCS_CUDA(wlcs::pair_fill(plan.d, plan.K, true, c.sms, c.stream));
+    if (c.timing) WLCS_CUDA(cudaEventRecord(c.ev1, c.stream));
+    const size_t maxlen = std::min(m, n);
+    WLCS_CUDA(c.outrev.ensure(maxlen + 16));
+    unsigned long long* zeros_dev = pair_zeros_ptr(c);
+    unsigned long long* dlen = zeros_dev + 1;
+    WLCS_CUDA(c.walk.ensure(wlcs::pair_walk_scratch_bytes(int64_t(m))));
+    uint32_t* dmiss = reinterpret_cast<uint32_t*>(zeros_dev + 2);
+    WLCS_CUDA(wlcs::pair_walk(plan.d, plan.K, dx, c.outrev.as<uint8_t>(), dlen, c.walk.p, dmiss,
+                              c.stream));
+    WLCS_CUDA(cudaMemcpyAsync(c.hscratch, dlen, 8, cudaMemcpyDeviceToHost, c.stream));
+    WLCS_CUDA(cudaMemcpyAsync(c.hscratch + 1, zeros_dev, 8, cudaMemcpyDeviceToHost, c.stream));
+    WLCS_CUDA(stream_wait(c.stream));
+    const unsigned long long len = c.hscratch[0], zeros = c.hscratch[1];
+    if (c.timing) {
+        WLCS_CUDA(cudaEventElapsedTime(&c.last_main_ms, c.ev0, c.ev1));
+        c.timing_pending = false;
+    }
+    if (env_int("WLCS_DEBUG_WALK", 0)) {
+        uint32_t miss[3] = {0, 0, 0};
+        WLCS_CUDA(cudaMemcpy(miss, dmiss, 12, cudaMemcpyDeviceToHost));
+        std::fprintf(stderr,
+                     "wlcs walk: %u of %lld blocks resolved by a fallback walk (resolve: %u of "
+                     "%u kcycles in fallbacks)\n",
+                     miss[0], (long long)((m + 255) / 256), miss[1], miss[2]);
+    }
+    if (len != zeros)
+        return fail(WLCS_E_INTERNAL, "traceback length " + std::to_string(len) +
+                                         " differs from the fill length " + std::to_string(zeros));
+    *len_out = len;
+    return WLCS_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -889,8 +1056,9 @@ int wlcs_length_device(const uint8_t* d_x, size_t m, const uint8_t* d_y, size_t 
     return pair_length_variant(*c, d_x, m, d_y, n, variant, out);
 }
 
-int wlcs_subsequence(const uint8_t* x, size_t m, const uint8_t* y, size_t n,
-                     size_t memory_budget, uint8_t* out, size_t cap, size_t* out_len) {
+int wlcs_subsequence_ex(const uint8_t* x, size_t m, const uint8_t* y, size_t n,
+                                   size_t memory_budget, size_t row_cap, uint8_t* out, size_t cap,
+                                   size_t* out_len) {
     if (!out_len) return fail(WLCS_E_INVALID_ARGUMENT, "out_len is NULL");
     if ((m && !x) || (n && !y)) return fail(WLCS_E_INVALID_ARGUMENT, "NULL input");
     int rc = capacity_check(m, n, memory_budget);
@@ -906,50 +1074,32 @@ int wlcs_subsequence(const uint8_t* x, size_t m, const uint8_t* y, size_t n,
     WLCS_CUDA(cudaMemcpyAsync(c->py.p, y, n, cudaMemcpyHostToDevice, c->stream));
     const uint8_t* dx = c->px.as<uint8_t>();
     const uint8_t* dy = c->py.as<uint8_t>();
-    // Orientation matters for tie-breaking: rows = x (parent), columns = y.
-    PairPlan plan;
-    rc = pair_setup(*c, dx, int64_t(m), dy, int64_t(n), true, plan);
+    // stored-row bytes of the full path (the strip plan's geometry, K = the
+    // cost model's choice for a store fill)
+    const int64_t W = (int64_t(n) + 31) / 32;
+    size_t limit = row_cap;
+    if (limit == 0) {
+        size_t free_b = 0, total_b = 0;
+        WLCS_CUDA(cudaMemGetInfo(&free_b, &total_b));
+        limit = std::min<size_t>(free_b / 2, size_t(8) << 30);
+    }
+    // full store needs about M * 32 * ceil(W / 32 / K) * K * 4 bytes >= M * N / 8
+    const double full_est = double(m + 528) * double((W + 31) / 32 * 32) * 4.0;
+    unsigned long long len = 0;
+    rc = full_est <= double(limit) ? subsequence_full(*c, dx, m, dy, n, &len)
+                                   : subsequence_banded(*c, dx, m, dy, n, limit, &len);
     if (rc) return rc;
-    if (c->timing && !c->ev0) {
-        WLCS_CUDA(cudaEventCreate(&c->ev0));
-        WLCS_CUDA(cudaEventCreate(&c->ev1));
-    }
-    if (c->timing) WLCS_CUDA(cudaEventRecord(c->ev0, c->stream));
-    WLCS_CUDA(wlcs::pair_fill(plan.d, plan.K, true, c->sms, c->stream));
-    if (c->timing) WLCS_CUDA(cudaEventRecord(c->ev1, c->stream));
-    const size_t maxlen = std::min(m, n);
-    WLCS_CUDA(c->outrev.ensure(maxlen + 16));
-    unsigned long long* zeros_dev = pair_zeros_ptr(*c);
-    unsigned long long* dlen = zeros_dev + 1;
-    WLCS_CUDA(c->walk.ensure(wlcs::pair_walk_scratch_bytes(int64_t(m))));
-    uint32_t* dmiss = reinterpret_cast<uint32_t*>(zeros_dev + 2);
-    WLCS_CUDA(wlcs::pair_walk(plan.d, plan.K, dx, c->outrev.as<uint8_t>(), dlen, c->walk.p,
-                              dmiss, c->stream));
-    WLCS_CUDA(cudaMemcpyAsync(c->hscratch, dlen, 8, cudaMemcpyDeviceToHost, c->stream));
-    WLCS_CUDA(cudaMemcpyAsync(c->hscratch + 1, zeros_dev, 8, cudaMemcpyDeviceToHost, c->stream));
-    WLCS_CUDA(stream_wait(c->stream));
-    const unsigned long long len = c->hscratch[0], zeros = c->hscratch[1];
-    if (c->timing) {
-        WLCS_CUDA(cudaEventElapsedTime(&c->last_main_ms, c->ev0, c->ev1));
-        c->timing_pending = false;
-    }
-    if (env_int("WLCS_DEBUG_WALK", 0)) {
-        uint32_t miss[3] = {0, 0, 0};
-        WLCS_CUDA(cudaMemcpy(miss, dmiss, 12, cudaMemcpyDeviceToHost));
-        std::fprintf(stderr,
-                     "wlcs walk: %u of %lld blocks resolved by a fallback walk (resolve: %u of "
-                     "%u kcycles in fallbacks)\n",
-                     miss[0], (long long)((m + 255) / 256), miss[1], miss[2]);
-    }
-    if (len != zeros)
-        return fail(WLCS_E_INTERNAL, "traceback length " + std::to_string(len) +
-                                         " differs from the fill length " + std::to_string(zeros));
     *out_len = size_t(len);
     if (len > cap)
         return fail(WLCS_E_INVALID_ARGUMENT, "output buffer holds " + std::to_string(cap) +
                                                  " bytes, subsequence has " + std::to_string(len));
     if (len) WLCS_CUDA(cudaMemcpy(out, c->outrev.p, len, cudaMemcpyDeviceToHost));
     return WLCS_OK;
+}
+
+int wlcs_subsequence(const uint8_t* x, size_t m, const uint8_t* y, size_t n,
+                     size_t memory_budget, uint8_t* out, size_t cap, size_t* out_len) {
+    return wlcs_subsequence_ex(x, m, y, n, memory_budget, 0, out, cap, out_len);
 }
 
 int wlcs_length_batch_device(const uint8_t* d_xs, const uint64_t* d_x_off, const uint8_t* d_ys,

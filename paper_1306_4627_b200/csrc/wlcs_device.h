@@ -93,6 +93,16 @@ struct FillProblem {
     // (the neighbour's inbox, a peer pointer); both [cwords] words, zeroed
     const uint32_t* ext_in;
     uint32_t* ext_out;
+    // banded (bounded-memory) traceback:
+    const uint32_t* v_in;   // optional: V words before the first row (a checkpoint); null = ones
+    uint32_t* ckpt_out;     // optional: V after every ckpt_chunks * 16 rows, [c - 1][W] for c >= 1
+    int ckpt_chunks;
+    int64_t walk_row0;      // global DP row of this problem's row 0 (walk's diagonal guess)
+    int64_t walk_mtot;      // rows of the whole pair (walk's diagonal guess)
+    int32_t* walk_entry;    // optional (device): entry column at the problem's last row, in:
+                            // the walk's exit column at its first row, out; null = N
+    unsigned long long* walk_place;  // optional (device): {LCS length, bytes already emitted
+                                     // by lower bands}; the walk writes its bytes before them
 };
 
 // One strip-kernel launch: up to kMaxProblems problems sharing the column

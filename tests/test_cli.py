@@ -82,10 +82,28 @@ def test_compute_fasta_and_whitespace(tmp_path):
 
 
 @pytest.mark.gpu
-def test_bench_csv(tmp_path):
+def test_bench_csv_gcups(tmp_path):
+    """--gcups: the device throughput schema (GCUPS, fraction of the int roofline)."""
     out = tmp_path / "b.csv"
-    rc, text = run("bench", "--sizes", "1000x1000,10000x10000", "--repetitions", "2", "--out", str(out))
+    rc, text = run("bench", "--gcups", "--sizes", "1000x1000,10000x10000", "--repetitions", "2",
+                   "--out", str(out))
     assert rc == 0
     rows = [l for l in out.read_text().splitlines() if l and not l.startswith("#")]
     assert rows[0] == "M,N,repetitions,device_s,gcups,roofline_frac,lcs_length"
     assert rows[2].split(",")[-1] == "6538"  # SURVEY 8(c) checkpoint, seed 1
+
+
+@pytest.mark.gpu
+def test_bench_csv_reference_schema(tmp_path):
+    """Default: the reference's bench (proj/src/bench.cpp:71-162) -- serial and
+    parallel fills with the equivalence gate, the 8-column CSV."""
+    out = tmp_path / "r.csv"
+    rc, text = run("bench", "--sizes", "10000x1000,100x10", "--workers", "1,4", "--repetitions", "1",
+                   "--seed", "1", "--out", str(out))
+    assert rc == 0, text
+    lines = out.read_text().splitlines()
+    assert lines[0] == "# wavelcs benchmark"
+    rows = [l for l in lines if l and not l.startswith("#")]
+    assert rows[0] == "M,N,workers,block_size,serial_s,parallel_s,speedup,lcs_length"
+    assert len(rows) == 5
+    assert rows[1].split(",")[-1] == rows[3].split(",")[-1]  # workers do not change the length

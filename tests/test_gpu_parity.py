@@ -637,3 +637,41 @@ def test_colsplit_concurrent_byte_alphabet(wl, restatement):
     x = a[np.minimum(rng.zipf(1.1, 5000), 256) - 1].tobytes()
     y = a[np.minimum(rng.zipf(1.1, 70_000), 256) - 1].tobytes()
     assert wl.colsplit_emulate(x, y, 3, 6) == restatement.length_bitpar(x, y)
+
+
+# ---- bounded-memory (banded) traceback --------------------------------------
+
+@pytest.mark.parametrize("m,n,alphabet,row_cap", [
+    (3000, 2500, DNA, 500_000), (5000, 700, PROTEIN, 300_000), (2000, 5000, DNA, 900_000),
+    (2049, 1999, b"AC", 400_000), (12000, 12000, DNA, 4 << 20), (8192, 130, DNA, 120_000)])
+def test_subsequence_banded_matches_reference(wl, restatement, m, n, alphabet, row_cap):
+    """With the traceback's device memory capped far below M * N / 8 the
+    string comes from row bands recomputed from checkpoints -- it must still
+    be the reference's traceback byte for byte (LEFT rule)."""
+    rng = np.random.default_rng(m * 31 + n)
+    a = np.frombuffer(alphabet, np.uint8)
+    x = a[rng.integers(0, len(a), m)].tobytes()
+    y = a[rng.integers(0, len(a), n)].tobytes()
+    assert row_cap < m * n // 8
+    assert wl.lcs_subsequence(x, y, wl.NO_BUDGET, row_cap=row_cap) == restatement.subsequence_bitrows(x, y)
+
+
+def test_golden_c3_subsequence_banded(wl):
+    """C3 (100k x ~100k mutated DNA; the full stored traceback needs 1.25 GB)
+    with a 24 MB cap: the reference's own traceback string (tests/golden)."""
+    import gzip
+    import json
+    import os
+    from paper_1306_4627_b200 import workloads
+    with gzip.open(os.path.join(os.path.dirname(__file__), "golden", "c3.json.gz"), "rt") as f:
+        data = json.load(f)
+    x, y = workloads.config_pair("c3")
+    sub = wl.lcs_subsequence(x, y, wl.NO_BUDGET, row_cap=24 << 20)
+    assert len(sub) == data["length"]
+    assert sub.decode() == data["subsequence"]
+
+
+def test_subsequence_cap_too_small(wl):
+    x = b"ACGT" * 5000
+    with pytest.raises(MemoryError):
+        wl.lcs_subsequence(x, x[::-1], wl.NO_BUDGET, row_cap=1000)
