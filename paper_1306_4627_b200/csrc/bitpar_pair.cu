@@ -210,8 +210,12 @@ __global__ void pair_code_rows_kernel(const uint8_t* row, int64_t rows, int reve
 //
 // Launch: 1-warp CTAs (one strip each), up to the occupancy limit (more
 // warps per CTA were measured: no gain, strips only share sub-partitions).
-template <int K, bool STORE>
+// MODE: 0 length, 1 store bit rows (traceback / tables / banded bands),
+// 3 length keeping a checkpoint V every ckpt_chunks chunks (banded
+// traceback, first pass)
+template <int K, int MODE>
 __global__ void __launch_bounds__(32, 1) pair_strip_kernel(PairDev d) {
+    constexpr bool STORE = MODE == 1, CKPT = MODE == 3;
     extern __shared__ __align__(16) uint8_t smem[];
     uint8_t* pm = smem;
     constexpr uint32_t cs = PmLayout<K>::code_stride;
@@ -242,8 +246,14 @@ __global__ void __launch_bounds__(32, 1) pair_strip_kernel(PairDev d) {
         const int64_t plane = P.plane;
         uint32_t V[K];
 #pragma unroll
-        for (int k = 0; k < K; ++k)
-            V[k] = (P.v_in && g * K + k < P.W) ? __ldg(P.v_in + g * K + k) : 0xffffffffu;
+        for (int k = 0; k < K; ++k) V[k] = 0xffffffffu;
+        if constexpr (STORE) {  // a band of the banded traceback starts at a checkpoint
+            if (P.v_in) {
+#pragma unroll
+                for (int k = 0; k < K; ++k)
+                    if (g * K + k < P.W) V[k] = __ldg(P.v_in + g * K + k);
+            }
+        }
         // the slice's first strip takes its carries from ext_in and its last
         // strip sends them to ext_out when the pair is split across GPUs
         const bool ext_left = strip == 0 && P.ext_in != nullptr;
@@ -358,7 +368,7 @@ __global__ void __launch_bounds__(32, 1) pair_strip_kernel(PairDev d) {
                 }
                 cin_lo = nl << 24;
                 cin_hi = nh << 24;
-                if (P.ckpt_out && valid && (ch + 1) % P.ckpt_chunks == 0 && ch + 1 < nchunks) {
+                if (CKPT && valid && (ch + 1) % P.ckpt_chunks == 0 && ch + 1 < nchunks) {
                     // checkpoint (ch + 1) / ckpt_chunks: V after the chunk's rows
                     uint32_t* c = P.ckpt_out + int64_t((ch + 1) / P.ckpt_chunks - 1) * P.W;
 #pragma unroll
@@ -970,17 +980,18 @@ cudaError_t pair_code_rows(const uint8_t* row, int64_t rows, bool reverse, const
     return cudaGetLastError();
 }
 
-template <int K, bool STORE>
+template <int K, int MODE>
 static cudaError_t launch_strip(const PairDev& dev, int sms, cudaStream_t stream) {
     PairDev d = dev;
     d.code_stride = uint32_t(pair_code_stride(K));
     d.pm_warp_bytes = uint32_t(d.sigma * pair_code_stride(K));
     const int smem = pair_smem_bytes(K, d.sigma);
-    cudaError_t e = cudaFuncSetAttribute(pair_strip_kernel<K, STORE>,
+    cudaError_t e = cudaFuncSetAttribute(pair_strip_kernel<K, MODE>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     int occ = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pair_strip_kernel<K, STORE>, 32, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pair_strip_kernel<K, MODE>, 32,
+                                                      smem);
     if (e != cudaSuccess) return e;
     if (occ < 1) occ = 1;
     int strips = 0;
@@ -990,20 +1001,25 @@ static cudaError_t launch_strip(const PairDev& dev, int sms, cudaStream_t stream
     if (d.max_ctas > 0 && grid > d.max_ctas) grid = d.max_ctas;
     if (grid * 32 > kPairSinkWords) grid = kPairSinkWords / 32;
     if (grid < d.nprob) grid = d.nprob;  // every problem needs a pool of at least one warp
-    pair_strip_kernel<K, STORE><<<grid, 32, smem, stream>>>(d);
+    pair_strip_kernel<K, MODE><<<grid, 32, smem, stream>>>(d);
     return cudaGetLastError();
 }
 
 cudaError_t pair_fill(const PairDev& d, int K, bool store, int sms, cudaStream_t stream) {
-    switch (K * 2 + (store ? 1 : 0)) {
-        case 2: return launch_strip<1, false>(d, sms, stream);
-        case 3: return launch_strip<1, true>(d, sms, stream);
-        case 4: return launch_strip<2, false>(d, sms, stream);
-        case 5: return launch_strip<2, true>(d, sms, stream);
-        case 8: return launch_strip<4, false>(d, sms, stream);
-        case 9: return launch_strip<4, true>(d, sms, stream);
-        case 16: return launch_strip<8, false>(d, sms, stream);
-        case 17: return launch_strip<8, true>(d, sms, stream);
+    const bool ckpt = !store && d.prob[0].ckpt_out != nullptr;
+    switch (K * 4 + (store ? 1 : ckpt ? 3 : 0)) {
+        case 4: return launch_strip<1, 0>(d, sms, stream);
+        case 5: return launch_strip<1, 1>(d, sms, stream);
+        case 7: return launch_strip<1, 3>(d, sms, stream);
+        case 8: return launch_strip<2, 0>(d, sms, stream);
+        case 9: return launch_strip<2, 1>(d, sms, stream);
+        case 11: return launch_strip<2, 3>(d, sms, stream);
+        case 16: return launch_strip<4, 0>(d, sms, stream);
+        case 17: return launch_strip<4, 1>(d, sms, stream);
+        case 19: return launch_strip<4, 3>(d, sms, stream);
+        case 32: return launch_strip<8, 0>(d, sms, stream);
+        case 33: return launch_strip<8, 1>(d, sms, stream);
+        case 35: return launch_strip<8, 3>(d, sms, stream);
         default: return cudaErrorInvalidValue;
     }
 }

@@ -229,14 +229,14 @@ int batch_pm_bytes() {  // >= flags + chunk stage; WLCS_BATCH_PM_KB overrides
     return kb > 0 ? std::max(kb, 14) * 1024 : 26880;
 }
 
-int choose_k(const Ctx& c, int64_t W, int64_t rows_per_prob, int sigma, int nprob) {
+int choose_k(const Ctx& c, int64_t W, int64_t rows_per_prob, const wlcs::PairDev& d, int nprob) {
     const int forced = env_int("WLCS_PAIR_K", 0);
     if (forced == 1 || forced == 2 || forced == 4 || forced == 8) return forced;
     const double chunks = double((rows_per_prob + 15) / 16);
     double best = 1e300;
     int best_k = 1;
     for (int K : {1, 2, 4, 8}) {
-        const int smem = wlcs::pair_smem_bytes(K, sigma);
+        const int smem = wlcs::pair_smem_bytes(K, d.sigma);
         if (smem > 200 * 1024) continue;
         const double step = K == 1 ? 330 : K == 2 ? 363 : K == 4 ? 535 : 987;
         const double strips = double((W + 32 * K - 1) / (32 * K));
@@ -293,7 +293,8 @@ int watchdog_read(Ctx& c, cudaStream_t s) {
     return WLCS_OK;
 }
 int watchdog_failed(Ctx& c) {
-    if (uint32_t(c.hscratch[7]) == 0) return WLCS_OK;
+    const uint32_t err = uint32_t(c.hscratch[7]);
+    if (err == 0) return WLCS_OK;
     return fail(WLCS_E_INTERNAL,
                 "strip kernel: carry words of a neighbouring slice never arrived (watchdog)");
 }
@@ -320,7 +321,7 @@ int pair_setup(Ctx& c, const uint8_t* d_row, int64_t rows, const uint8_t* d_col,
     WLCS_CUDA(wlcs::pair_prepare(d, present, map, sigma_dev, c.stream, &sigma));
     const int64_t W = (cols + 31) / 32;
     const int64_t mid = split ? rows / 2 : rows;
-    plan.K = choose_k(c, W, rows - mid > mid ? rows - mid : mid, sigma, d.nprob);
+    plan.K = choose_k(c, W, rows - mid > mid ? rows - mid : mid, d, d.nprob);
     if (wlcs::pair_smem_bytes(plan.K, sigma) > 220 * 1024)
         return fail(WLCS_E_INTERNAL, "match-mask table does not fit in shared memory");
     const int K = plan.K;
@@ -727,7 +728,7 @@ extern "C" int wlcs_colsplit_emulate(const uint8_t* x, size_t m, const uint8_t* 
     const int64_t mid = int64_t(m / 2);
     int64_t wmax = 0;
     for (int g = 0; g < G; ++g) wmax = std::max<int64_t>(wmax, int64_t(hi[g] - lo[g] + 31) / 32);
-    const int K = choose_k(*c, wmax, int64_t(m) - mid, sigma, 2 * G);
+    const int K = choose_k(*c, wmax, int64_t(m) - mid, d, 2 * G);
     if (wlcs::pair_smem_bytes(K, sigma) > 220 * 1024)
         return fail(WLCS_E_INTERNAL, "match-mask table does not fit in shared memory");
     d.nprob = 2 * G;
@@ -1317,7 +1318,7 @@ int wlcs_colsplit_fill(const uint8_t* x, size_t m, const uint8_t* y, size_t n, s
     const bool want[2] = {(problems & WLCS_COLSPLIT_FORWARD) != 0,
                           (problems & WLCS_COLSPLIT_REVERSE) != 0};
     d.nprob = (want[0] ? 1 : 0) + (want[1] ? 1 : 0);
-    const int K = choose_k(*c, W, int64_t(m) - mid, sigma, d.nprob);
+    const int K = choose_k(*c, W, int64_t(m) - mid, d, d.nprob);
     if (wlcs::pair_smem_bytes(K, sigma) > 220 * 1024)
         return fail(WLCS_E_INTERNAL, "match-mask table does not fit in shared memory");
     const size_t pm_words = size_t(sigma) * size_t(W);

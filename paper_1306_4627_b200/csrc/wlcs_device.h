@@ -143,6 +143,7 @@ cudaError_t pair_reverse(const uint8_t* src, int64_t n, uint8_t* dst, cudaStream
 cudaError_t pair_split_combine(const uint32_t* vf, const uint32_t* vr, int64_t W, int64_t N,
                                uint32_t* scratch, unsigned long long* best, cudaStream_t stream);
 int pair_smem_bytes(int K, int sigma);
+
 cudaError_t pair_fill(const PairDev& d, int K, bool store, int sms, cudaStream_t stream);
 // The reference's DpTable / BacktrackTable from the stored bit rows.
 cudaError_t pair_tables(const PairDev& d, int K, uint32_t* dp, uint8_t* back,
