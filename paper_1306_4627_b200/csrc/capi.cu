@@ -220,9 +220,16 @@ struct PairPlan {
 // Lane shapes up to K = 10 words per lane in 26.25 KB of masks per warp
 // (21 codes x 1280 B: the 20-letter alphabet plus the zero row) -> 8 warps
 // per SM, two per sub-partition.
-int batch_kmax() {
-    const int k = env_int("WLCS_BATCH_KMAX", 10);
-    return k >= 1 && k <= 12 ? k : 10;
+// Small batches (e.g. one GPU's shard of a strong-scaling run) are bound by
+// their longest task, not by throughput: narrower lane shapes (more lanes per
+// pair, shorter tasks) win there.  Measured on C2-like pairs (tools/gpu/
+// small_batch.sh): 8,192 pairs best at kmax 6, 16-32k at 8, 65,536 at 10.
+int batch_kmax(size_t pairs = 0) {
+    const int k = env_int("WLCS_BATCH_KMAX", 0);
+    if (k >= 1 && k <= 12) return k;
+    if (pairs && pairs <= 12288) return 6;
+    if (pairs && pairs <= 40960) return 8;
+    return 10;
 }
 int batch_pm_bytes() {  // >= flags + chunk stage; WLCS_BATCH_PM_KB overrides
     const int kb = env_int("WLCS_BATCH_PM_KB", 0);
@@ -488,7 +495,7 @@ bool batch_is_long(uint64_t m, uint64_t n, int kmax) {
 int batch_enqueue(Ctx& c, const uint8_t* d_xs, const uint64_t* d_xoff, const uint8_t* d_ys,
                   const uint64_t* d_yoff, size_t pairs, uint64_t xs_bytes, uint64_t ys_bytes,
                   uint32_t* d_out, cudaStream_t s, void* ws, bool long_to_host, bool ev_start,
-                  bool ev_end) {
+                  bool ev_end, int kmax) {
     if (pairs == 0) return WLCS_OK;
     wlcs::BatchDev d{};
     d.xs = d_xs;
@@ -500,7 +507,7 @@ int batch_enqueue(Ctx& c, const uint8_t* d_xs, const uint64_t* d_xoff, const uin
     d.out = d_out;
     d.pairs = uint32_t(pairs);
     d.pm_bytes = batch_pm_bytes();
-    d.kmax = batch_kmax();
+    d.kmax = kmax;  // the host's long-pair routing used the same value
     d.long_to_host = long_to_host ? 1 : 0;
     if ((ev_start || ev_end) && !c.ev0) {
         WLCS_CUDA(cudaEventCreate(&c.ev0));
@@ -591,7 +598,8 @@ int batch_wave(Ctx& c, const uint8_t* d_xs, const uint64_t* d_xoff, const uint8_
 // workspace is reused in stream order).  Pairs wider than the first pass's
 // lane shapes are finished afterwards by the strip kernel (batch_long_pairs).
 int batch_host_pipelined(Ctx& c, const uint8_t* xs, const uint64_t* x_off, const uint8_t* ys,
-                         const uint64_t* y_off, size_t pairs, int nchunks, uint32_t* out) {
+                         const uint64_t* y_off, size_t pairs, int nchunks, int kmax,
+                         uint32_t* out) {
     const uint64_t xs_bytes = x_off[pairs], ys_bytes = y_off[pairs];
     if (!c.copy_stream) WLCS_CUDA(cudaStreamCreateWithFlags(&c.copy_stream, cudaStreamNonBlocking));
     while (int(c.chunk_ev.size()) < nchunks) {
@@ -623,7 +631,7 @@ int batch_host_pipelined(Ctx& c, const uint8_t* xs, const uint64_t* x_off, const
                                    c.yoff.as<uint64_t>() + p0[k], p0[k + 1] - p0[k], xs_bytes,
                                    ys_bytes, c.out.as<uint32_t>() + p0[k], s,
                                    c.ws.as<uint8_t>() + ws_off[k], true,
-                                   c.timing && k == 0, c.timing && k == nchunks - 1))
+                                   c.timing && k == 0, c.timing && k == nchunks - 1, kmax))
             return rc;
     }
     WLCS_CUDA(cudaMemcpyAsync(out, c.out.p, pairs * 4, cudaMemcpyDeviceToHost, s));
@@ -1123,7 +1131,7 @@ int wlcs_length_batch_device(const uint8_t* d_xs, const uint64_t* d_x_off, const
     }
     WLCS_CUDA(c->ws.ensure(wlcs::batch_workspace_bytes(uint32_t(pairs), batch_pm_bytes())));
     return batch_enqueue(*c, d_xs, d_x_off, d_ys, d_y_off, pairs, xs_bytes, ys_bytes, d_out, s,
-                         c->ws.p, false, c->timing, c->timing);
+                         c->ws.p, false, c->timing, c->timing, batch_kmax(pairs));
 }
 
 int wlcs_length_batch_ex(const uint8_t* xs, const uint64_t* x_off, const uint8_t* ys,
@@ -1151,8 +1159,8 @@ int wlcs_length_batch_ex(const uint8_t* xs, const uint64_t* x_off, const uint8_t
     // pairs too wide for the first pass's lane shapes: strip kernel (the
     // host knows the offsets, so they never reach the device second pass)
     std::vector<size_t> long_ids;
+    const int kmax = batch_kmax(pairs);
     if (variant == WLCS_VARIANT_BITPARALLEL) {
-        const int kmax = batch_kmax();
         for (size_t k = 0; k < pairs; ++k)
             if (batch_is_long(x_off[k + 1] - x_off[k], y_off[k + 1] - y_off[k], kmax))
                 long_ids.push_back(k);
@@ -1162,7 +1170,7 @@ int wlcs_length_batch_ex(const uint8_t* xs, const uint64_t* x_off, const uint8_t
                                                    pairs / 8192))
                             : 1;
     if (nchunks >= 2 && xs_bytes + ys_bytes >= (16u << 20)) {
-        rc = batch_host_pipelined(*c, xs, x_off, ys, y_off, pairs, nchunks, out);
+        rc = batch_host_pipelined(*c, xs, x_off, ys, y_off, pairs, nchunks, kmax, out);
         if (rc) return rc;
         return batch_long_pairs(*c, c->xs.as<uint8_t>(), c->ys.as<uint8_t>(), x_off, y_off,
                                 long_ids, out);
@@ -1178,7 +1186,7 @@ int wlcs_length_batch_ex(const uint8_t* xs, const uint64_t* x_off, const uint8_t
         WLCS_CUDA(c->ws.ensure(wlcs::batch_workspace_bytes(uint32_t(pairs), batch_pm_bytes())));
         rc = batch_enqueue(*c, c->xs.as<uint8_t>(), c->xoff.as<uint64_t>(), c->ys.as<uint8_t>(),
                            c->yoff.as<uint64_t>(), pairs, xs_bytes, ys_bytes,
-                           c->out.as<uint32_t>(), s, c->ws.p, true, c->timing, c->timing);
+                           c->out.as<uint32_t>(), s, c->ws.p, true, c->timing, c->timing, kmax);
     }
     if (rc) return rc;
     WLCS_CUDA(cudaMemcpyAsync(out, c->out.p, pairs * 4, cudaMemcpyDeviceToHost, s));
