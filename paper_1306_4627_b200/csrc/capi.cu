@@ -91,6 +91,9 @@ struct Ctx {
     // copy (~10 us) inside the caller's timed region
     uint64_t* hscratch = nullptr;
     cudaEvent_t join_ev = nullptr;       // orders c.stream after a caller's stream
+    // pinned staging ring for host->device copies of pageable caller buffers
+    uint8_t* hstage[2] = {nullptr, nullptr};
+    cudaEvent_t stage_ev[2] = {nullptr, nullptr};
     // batch (ws: first pass per chunk; ws2 + wcarry: the device second pass)
     DevBuf xs, ys, xoff, yoff, out, ws, ws2, wcarry;
     // single pair
@@ -100,6 +103,10 @@ struct Ctx {
         if (hscratch) cudaFreeHost(hscratch);
         for (cudaEvent_t e : chunk_ev) cudaEventDestroy(e);
         if (join_ev) cudaEventDestroy(join_ev);
+        for (int i = 0; i < 2; ++i) {
+            if (hstage[i]) cudaFreeHost(hstage[i]);
+            if (stage_ev[i]) cudaEventDestroy(stage_ev[i]);
+        }
         if (copy_stream) cudaStreamDestroy(copy_stream);
         if (stream) cudaStreamDestroy(stream);
     }
@@ -179,6 +186,44 @@ int join_caller(Ctx& c, cudaStream_t user) {
     if (!c.join_ev) WLCS_CUDA(cudaEventCreateWithFlags(&c.join_ev, cudaEventDisableTiming));
     WLCS_CUDA(cudaEventRecord(c.join_ev, user));
     WLCS_CUDA(cudaStreamWaitEvent(c.stream, c.join_ev, 0));
+    return WLCS_OK;
+}
+
+// Host -> device copy of a caller's buffer (the input path of the single-pair
+// entry points).  Page-locked sources (wlcs_host_alloc, cudaHostAlloc) are
+// copied directly; pageable ones go through a ring of two 4 MB pinned stage
+// buffers, the host memcpy of chunk k+1 overlapping the DMA of chunk k (a
+// stage is reused only after its previous DMA finished: its event).  Small
+// copies go straight to the driver.
+constexpr size_t kStageBytes = size_t(4) << 20;
+int h2d_staged(Ctx& c, void* dst, const void* src, size_t n, cudaStream_t s) {
+    if (n == 0) return WLCS_OK;
+    cudaPointerAttributes attr{};
+    const bool pinned = cudaPointerGetAttributes(&attr, src) == cudaSuccess &&
+                        (attr.type == cudaMemoryTypeHost || attr.type == cudaMemoryTypeManaged);
+    cudaGetLastError();
+    if (pinned || n <= (size_t(64) << 10)) {
+        WLCS_CUDA(cudaMemcpyAsync(dst, src, n, cudaMemcpyHostToDevice, s));
+        return WLCS_OK;
+    }
+    for (int i = 0; i < 2; ++i) {
+        if (!c.hstage[i]) WLCS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&c.hstage[i]), kStageBytes,
+                                                  cudaHostAllocDefault));
+        if (!c.stage_ev[i]) {
+            WLCS_CUDA(cudaEventCreateWithFlags(&c.stage_ev[i], cudaEventDisableTiming));
+            WLCS_CUDA(cudaEventRecord(c.stage_ev[i], s));
+        }
+    }
+    const uint8_t* from = static_cast<const uint8_t*>(src);
+    uint8_t* to = static_cast<uint8_t*>(dst);
+    for (size_t off = 0, k = 0; off < n; off += kStageBytes, ++k) {
+        const size_t len = std::min(kStageBytes, n - off);
+        const int i = int(k & 1);
+        WLCS_CUDA(cudaEventSynchronize(c.stage_ev[i]));  // its previous DMA is done
+        std::memcpy(c.hstage[i], from + off, len);
+        WLCS_CUDA(cudaMemcpyAsync(to + off, c.hstage[i], len, cudaMemcpyHostToDevice, s));
+        WLCS_CUDA(cudaEventRecord(c.stage_ev[i], s));
+    }
     return WLCS_OK;
 }
 
@@ -706,8 +751,8 @@ extern "C" int wlcs_colsplit_emulate(const uint8_t* x, size_t m, const uint8_t* 
     WLCS_CUDA(c->px.ensure(m + 16));
     WLCS_CUDA(c->py.ensure(n + 16));
     WLCS_CUDA(c->ry.ensure(n + 16));
-    WLCS_CUDA(cudaMemcpyAsync(c->px.p, x, m, cudaMemcpyHostToDevice, c->stream));
-    WLCS_CUDA(cudaMemcpyAsync(c->py.p, y, n, cudaMemcpyHostToDevice, c->stream));
+    if (int rc_ = h2d_staged(*c, c->px.p, x, m, c->stream)) return rc_;
+    if (int rc_ = h2d_staged(*c, c->py.p, y, n, c->stream)) return rc_;
     const uint8_t* dx = c->px.as<uint8_t>();
     const uint8_t* dy = c->py.as<uint8_t>();
     uint8_t* dry = c->ry.as<uint8_t>();
@@ -1037,8 +1082,8 @@ int wlcs_length_ex(const uint8_t* x, size_t m, const uint8_t* y, size_t n, size_
     }
     WLCS_CUDA(c->px.ensure(m + 16));
     WLCS_CUDA(c->py.ensure(n + 16));
-    WLCS_CUDA(cudaMemcpyAsync(c->px.p, x, m, cudaMemcpyHostToDevice, c->stream));
-    WLCS_CUDA(cudaMemcpyAsync(c->py.p, y, n, cudaMemcpyHostToDevice, c->stream));
+    if (int rc_ = h2d_staged(*c, c->px.p, x, m, c->stream)) return rc_;
+    if (int rc_ = h2d_staged(*c, c->py.p, y, n, c->stream)) return rc_;
     const uint8_t* dx = c->px.as<uint8_t>();
     const uint8_t* dy = c->py.as<uint8_t>();
     return pair_length_variant(*c, dx, m, dy, n, variant, out);
@@ -1079,8 +1124,8 @@ int wlcs_subsequence_ex(const uint8_t* x, size_t m, const uint8_t* y, size_t n,
     if (m == 0 || n == 0) return WLCS_OK;
     WLCS_CUDA(c->px.ensure(m + 16));
     WLCS_CUDA(c->py.ensure(n + 16));
-    WLCS_CUDA(cudaMemcpyAsync(c->px.p, x, m, cudaMemcpyHostToDevice, c->stream));
-    WLCS_CUDA(cudaMemcpyAsync(c->py.p, y, n, cudaMemcpyHostToDevice, c->stream));
+    if (int rc_ = h2d_staged(*c, c->px.p, x, m, c->stream)) return rc_;
+    if (int rc_ = h2d_staged(*c, c->py.p, y, n, c->stream)) return rc_;
     const uint8_t* dx = c->px.as<uint8_t>();
     const uint8_t* dy = c->py.as<uint8_t>();
     // stored-row bytes of the full path (the strip plan's geometry, K = the
@@ -1303,9 +1348,8 @@ int wlcs_colsplit_fill(const uint8_t* x, size_t m, const uint8_t* y, size_t n, s
     const int64_t W = (cols + 31) / 32;
     WLCS_CUDA(c->px.ensure(m + 16));
     WLCS_CUDA(c->py.ensure(size_t(cols) + 16));
-    WLCS_CUDA(cudaMemcpyAsync(c->px.p, x, m, cudaMemcpyHostToDevice, c->stream));
-    WLCS_CUDA(cudaMemcpyAsync(c->py.p, y + col_lo, size_t(cols), cudaMemcpyHostToDevice,
-                              c->stream));
+    if (int rc_ = h2d_staged(*c, c->px.p, x, m, c->stream)) return rc_;
+    if (int rc_ = h2d_staged(*c, c->py.p, y + col_lo, size_t(cols), c->stream)) return rc_;
     const uint8_t* dx = c->px.as<uint8_t>();
     const uint8_t* dcol = c->py.as<uint8_t>();
     wlcs::PairDev d{};
@@ -1588,8 +1632,8 @@ int wlcs_fill_tables(const uint8_t* x, size_t m, const uint8_t* y, size_t n,
     }
     WLCS_CUDA(c->px.ensure(m + 16));
     WLCS_CUDA(c->py.ensure(n + 16));
-    WLCS_CUDA(cudaMemcpyAsync(c->px.p, x, m, cudaMemcpyHostToDevice, c->stream));
-    WLCS_CUDA(cudaMemcpyAsync(c->py.p, y, n, cudaMemcpyHostToDevice, c->stream));
+    if (int rc_ = h2d_staged(*c, c->px.p, x, m, c->stream)) return rc_;
+    if (int rc_ = h2d_staged(*c, c->py.p, y, n, c->stream)) return rc_;
     PairPlan plan;
     rc = pair_setup(*c, c->px.as<uint8_t>(), int64_t(m), c->py.as<uint8_t>(), int64_t(n), true,
                     plan);

@@ -675,3 +675,33 @@ def test_subsequence_cap_too_small(wl):
     x = b"ACGT" * 5000
     with pytest.raises(MemoryError):
         wl.lcs_subsequence(x, x[::-1], wl.NO_BUDGET, row_cap=1000)
+
+
+def test_batch_c2_full_against_oracle(wl, restatement):
+    """The whole C2 batch (65,536 protein pairs, BASELINE configs[1]) through
+    the host entry point against the oracle's lengths -- every pair, not a
+    sample (the bench's equivalence gate runs on the reference's sample)."""
+    xs, xo, ys, yo = restatement.generate_pairs(65536, 200, 1000, PROTEIN, 20130619)
+    got = wl.lcs_length_batch(xs[: xo[-1]], xo, ys[: yo[-1]], yo)
+    want = restatement.length_batch(xs, xo, ys, yo)
+    assert np.array_equal(got, want)
+
+
+def test_single_pair_pageable_and_pinned_inputs(wl, restatement):
+    """Single-pair H2D goes through the pinned stage ring for pageable
+    buffers larger than one 4 MB stage; page-locked buffers go direct."""
+    import ctypes as ct
+    rng = np.random.default_rng(8)
+    x = rng.choice(np.frombuffer(DNA, np.uint8), 9_000_000).tobytes()
+    y = rng.choice(np.frombuffer(DNA, np.uint8), 3000).tobytes()
+    want = restatement.length_bitpar(x, y)
+    assert wl.lcs_length(x, y, wl.NO_BUDGET) == want
+    p = wl.lib.wlcs_host_alloc(len(x))
+    try:
+        ct.memmove(p, x, len(x))
+        out = ct.c_uint32()
+        wl._check(wl.lib.wlcs_length_ex(p, len(x), y, len(y), wl.NO_BUDGET, wl.VARIANT_BITPARALLEL,
+                                        ct.byref(out)))
+        assert out.value == want
+    finally:
+        wl.lib.wlcs_host_free(ct.c_void_p(p))
