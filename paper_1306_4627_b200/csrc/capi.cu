@@ -640,11 +640,17 @@ int batch_wave(Ctx& c, const uint8_t* d_xs, const uint64_t* d_xoff, const uint8_
 // the pairs are cut into nchunks contiguous chunks; chunk k's string bytes are
 // copied on copy_stream while chunk k-1 runs on the compute stream (its own
 // first-pass workspace, so the chunks' plans never overlap; the second pass's
-// workspace is reused in stream order).  Pairs wider than the first pass's
-// lane shapes are finished afterwards by the strip kernel (batch_long_pairs).
-int batch_host_pipelined(Ctx& c, const uint8_t* xs, const uint64_t* x_off, const uint8_t* ys,
-                         const uint64_t* y_off, size_t pairs, int nchunks, int kmax,
-                         uint32_t* out) {
+// workspace is reused in stream order).  All copies are enqueued first and the
+// offsets are validated on the host while they run (copy extents are clamped
+// to the buffers, so invalid offsets cannot write outside them; nothing is
+// computed before the check).  Pairs wider than the first pass's lane shapes
+// are finished afterwards by the strip kernel (batch_long_pairs).
+struct PipePlan {
+    std::vector<size_t> p0, ws_off;
+};
+
+int batch_pipe_copies(Ctx& c, const uint8_t* xs, const uint64_t* x_off, const uint8_t* ys,
+                      const uint64_t* y_off, size_t pairs, int nchunks, PipePlan& pp) {
     const uint64_t xs_bytes = x_off[pairs], ys_bytes = y_off[pairs];
     if (!c.copy_stream) WLCS_CUDA(cudaStreamCreateWithFlags(&c.copy_stream, cudaStreamNonBlocking));
     while (int(c.chunk_ev.size()) < nchunks) {
@@ -653,34 +659,74 @@ int batch_host_pipelined(Ctx& c, const uint8_t* xs, const uint64_t* x_off, const
         c.chunk_ev.push_back(e);
     }
     const int pm_bytes = batch_pm_bytes();
-    std::vector<size_t> p0(nchunks + 1);
-    for (int k = 0; k <= nchunks; ++k) p0[k] = pairs * size_t(k) / size_t(nchunks);
-    std::vector<size_t> ws_off(nchunks + 1, 0);
+    pp.p0.assign(nchunks + 1, 0);
+    for (int k = 0; k <= nchunks; ++k) pp.p0[k] = pairs * size_t(k) / size_t(nchunks);
+    pp.ws_off.assign(nchunks + 1, 0);
     for (int k = 0; k < nchunks; ++k)
-        ws_off[k + 1] = ws_off[k] + ((wlcs::batch_workspace_bytes(uint32_t(p0[k + 1] - p0[k]),
-                                                                  pm_bytes) + 255) & ~size_t(255));
-    WLCS_CUDA(c.ws.ensure(ws_off[nchunks]));
-    cudaStream_t cs = c.copy_stream, s = c.stream;
+        pp.ws_off[k + 1] = pp.ws_off[k] + ((wlcs::batch_workspace_bytes(
+                                                uint32_t(pp.p0[k + 1] - pp.p0[k]), pm_bytes) +
+                                            255) & ~size_t(255));
+    WLCS_CUDA(c.ws.ensure(pp.ws_off[nchunks]));
+    cudaStream_t cs = c.copy_stream;
     uint8_t* dxs = c.xs.as<uint8_t>();
     uint8_t* dys = c.ys.as<uint8_t>();
     WLCS_CUDA(cudaMemcpyAsync(c.xoff.p, x_off, (pairs + 1) * 8, cudaMemcpyHostToDevice, cs));
     WLCS_CUDA(cudaMemcpyAsync(c.yoff.p, y_off, (pairs + 1) * 8, cudaMemcpyHostToDevice, cs));
     for (int k = 0; k < nchunks; ++k) {
-        const uint64_t xa = x_off[p0[k]], xb = x_off[p0[k + 1]];
-        const uint64_t ya = y_off[p0[k]], yb = y_off[p0[k + 1]];
+        const uint64_t xa = std::min(x_off[pp.p0[k]], xs_bytes);
+        const uint64_t xb = std::min(x_off[pp.p0[k + 1]], xs_bytes);
+        const uint64_t ya = std::min(y_off[pp.p0[k]], ys_bytes);
+        const uint64_t yb = std::min(y_off[pp.p0[k + 1]], ys_bytes);
         if (xb > xa) WLCS_CUDA(cudaMemcpyAsync(dxs + xa, xs + xa, xb - xa, cudaMemcpyHostToDevice, cs));
         if (yb > ya) WLCS_CUDA(cudaMemcpyAsync(dys + ya, ys + ya, yb - ya, cudaMemcpyHostToDevice, cs));
         WLCS_CUDA(cudaEventRecord(c.chunk_ev[k], cs));
+    }
+    return WLCS_OK;
+}
+
+int batch_pipe_compute(Ctx& c, const uint64_t* x_off, const uint64_t* y_off, size_t pairs,
+                       int nchunks, int kmax, const PipePlan& pp, uint32_t* out) {
+    const uint64_t xs_bytes = x_off[pairs], ys_bytes = y_off[pairs];
+    cudaStream_t s = c.stream;
+    for (int k = 0; k < nchunks; ++k) {
         WLCS_CUDA(cudaStreamWaitEvent(s, c.chunk_ev[k], 0));
-        if (int rc = batch_enqueue(c, dxs, c.xoff.as<uint64_t>() + p0[k], dys,
-                                   c.yoff.as<uint64_t>() + p0[k], p0[k + 1] - p0[k], xs_bytes,
-                                   ys_bytes, c.out.as<uint32_t>() + p0[k], s,
-                                   c.ws.as<uint8_t>() + ws_off[k], true,
-                                   c.timing && k == 0, c.timing && k == nchunks - 1, kmax))
+        if (int rc = batch_enqueue(c, c.xs.as<uint8_t>(), c.xoff.as<uint64_t>() + pp.p0[k],
+                                   c.ys.as<uint8_t>(), c.yoff.as<uint64_t>() + pp.p0[k],
+                                   pp.p0[k + 1] - pp.p0[k], xs_bytes, ys_bytes,
+                                   c.out.as<uint32_t>() + pp.p0[k], s,
+                                   c.ws.as<uint8_t>() + pp.ws_off[k], true, c.timing && k == 0,
+                                   c.timing && k == nchunks - 1, kmax))
             return rc;
     }
     WLCS_CUDA(cudaMemcpyAsync(out, c.out.p, pairs * 4, cudaMemcpyDeviceToHost, s));
     WLCS_CUDA(stream_wait(s));
+    return WLCS_OK;
+}
+
+// One pass over both offset arrays: non-decreasing (std::invalid_argument
+// otherwise) and the pairs too wide for the first pass's lane shapes.
+int scan_offsets(const uint64_t* x_off, const uint64_t* y_off, size_t pairs, int kmax,
+                 bool want_long, std::vector<size_t>& long_ids) {
+    const uint64_t lim = uint64_t(32) * 32 * uint64_t(kmax);  // columns of 32 * kmax words
+    bool bad = false, any_long = false;
+    for (size_t k = 0; k < pairs; ++k) {
+        const uint64_t m = x_off[k + 1] - x_off[k], n = y_off[k + 1] - y_off[k];
+        bad |= (x_off[k + 1] < x_off[k]) | (y_off[k + 1] < y_off[k]);
+        any_long |= (m < n ? m : n) > lim;
+    }
+    if (bad) {
+        for (size_t k = 0; k < pairs; ++k) {
+            if (x_off[k + 1] < x_off[k])
+                return fail(WLCS_E_INVALID_ARGUMENT, "x offsets decrease at pair " + std::to_string(k));
+            if (y_off[k + 1] < y_off[k])
+                return fail(WLCS_E_INVALID_ARGUMENT, "y offsets decrease at pair " + std::to_string(k));
+        }
+    }
+    long_ids.clear();
+    if (want_long && any_long)
+        for (size_t k = 0; k < pairs; ++k)
+            if (batch_is_long(x_off[k + 1] - x_off[k], y_off[k + 1] - y_off[k], kmax))
+                long_ids.push_back(k);
     return WLCS_OK;
 }
 
@@ -1186,12 +1232,8 @@ int wlcs_length_batch_ex(const uint8_t* xs, const uint64_t* x_off, const uint8_t
     if (pairs > 0x7fffffffull) return fail(WLCS_E_INVALID_ARGUMENT, "too many pairs in one batch");
     if (variant != WLCS_VARIANT_BITPARALLEL && variant != WLCS_VARIANT_WAVEFRONT)
         return fail(WLCS_E_CONFIG, "unknown fill variant " + std::to_string(variant));
-    int rc = validate_offsets(x_off, pairs, "x");
-    if (rc) return rc;
-    rc = validate_offsets(y_off, pairs, "y");
-    if (rc) return rc;
     Ctx* c = nullptr;
-    rc = get_ctx(&c);
+    int rc = get_ctx(&c);
     if (rc) return rc;
     const uint64_t xs_bytes = x_off[pairs], ys_bytes = y_off[pairs];
     if ((xs_bytes && !xs) || (ys_bytes && !ys)) return fail(WLCS_E_INVALID_ARGUMENT, "NULL strings");
@@ -1201,30 +1243,36 @@ int wlcs_length_batch_ex(const uint8_t* xs, const uint64_t* x_off, const uint8_t
     WLCS_CUDA(c->yoff.ensure((pairs + 1) * 8));
     WLCS_CUDA(c->out.ensure(pairs * 4));
     cudaStream_t s = c->stream;
-    // pairs too wide for the first pass's lane shapes: strip kernel (the
-    // host knows the offsets, so they never reach the device second pass)
+    // pairs too wide for the first pass's lane shapes go to the strip kernel
+    // (the host knows the offsets, so they never reach the device second pass)
     std::vector<size_t> long_ids;
     const int kmax = batch_kmax(pairs);
-    if (variant == WLCS_VARIANT_BITPARALLEL) {
-        for (size_t k = 0; k < pairs; ++k)
-            if (batch_is_long(x_off[k + 1] - x_off[k], y_off[k + 1] - y_off[k], kmax))
-                long_ids.push_back(k);
-    }
-    const int nchunks = variant == WLCS_VARIANT_BITPARALLEL
-                            ? int(std::min<size_t>(std::min<size_t>(size_t(env_int("WLCS_BATCH_CHUNKS", 4)), 64),
-                                                   pairs / 8192))
-                            : 1;
+    const bool bitpar = variant == WLCS_VARIANT_BITPARALLEL;
+    const int nchunks =
+        bitpar ? int(std::min<size_t>(std::min<size_t>(size_t(env_int("WLCS_BATCH_CHUNKS", 4)), 64),
+                                      pairs / 8192))
+               : 1;
     if (nchunks >= 2 && xs_bytes + ys_bytes >= (16u << 20)) {
-        rc = batch_host_pipelined(*c, xs, x_off, ys, y_off, pairs, nchunks, kmax, out);
+        PipePlan pp;
+        rc = batch_pipe_copies(*c, xs, x_off, ys, y_off, pairs, nchunks, pp);
+        if (rc) return rc;
+        rc = scan_offsets(x_off, y_off, pairs, kmax, true, long_ids);  // while the DMA runs
+        if (rc) {
+            cudaStreamSynchronize(c->copy_stream);  // the copies read the caller's buffers
+            return rc;
+        }
+        rc = batch_pipe_compute(*c, x_off, y_off, pairs, nchunks, kmax, pp, out);
         if (rc) return rc;
         return batch_long_pairs(*c, c->xs.as<uint8_t>(), c->ys.as<uint8_t>(), x_off, y_off,
                                 long_ids, out);
     }
+    rc = scan_offsets(x_off, y_off, pairs, kmax, bitpar, long_ids);
+    if (rc) return rc;
     if (xs_bytes) WLCS_CUDA(cudaMemcpyAsync(c->xs.p, xs, xs_bytes, cudaMemcpyHostToDevice, s));
     if (ys_bytes) WLCS_CUDA(cudaMemcpyAsync(c->ys.p, ys, ys_bytes, cudaMemcpyHostToDevice, s));
     WLCS_CUDA(cudaMemcpyAsync(c->xoff.p, x_off, (pairs + 1) * 8, cudaMemcpyHostToDevice, s));
     WLCS_CUDA(cudaMemcpyAsync(c->yoff.p, y_off, (pairs + 1) * 8, cudaMemcpyHostToDevice, s));
-    if (variant == WLCS_VARIANT_WAVEFRONT) {
+    if (!bitpar) {
         rc = batch_wave(*c, c->xs.as<uint8_t>(), c->xoff.as<uint64_t>(), c->ys.as<uint8_t>(),
                         c->yoff.as<uint64_t>(), pairs, c->out.as<uint32_t>(), s);
     } else {
