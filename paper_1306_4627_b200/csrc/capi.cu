@@ -487,7 +487,9 @@ int pair_wave_device(Ctx& c, const uint8_t* dx, size_t m, const uint8_t* dy, siz
     if (d.n >= (int64_t(1) << 24))
         return fail(WLCS_E_CONFIG, "wavefront variant: the shorter string must be < 2^24 bytes");
     d.bstride = ((d.n + 64) + 31) & ~int64_t(31);
-    const int64_t bands = wlcs::wave_pair_bands(d.m);
+    d.R = wlcs::wave_pair_rows(d.m, c.sms);
+    if (const char* e = std::getenv("WLCS_WAVE_PAIR_R")) d.R = std::atoi(e);  // experiments
+    const int64_t bands = wlcs::wave_pair_bands(d.m, d.R);
     const int64_t budget = int64_t(1) << 30;  // boundary-row ring
     int64_t nbuf = budget / (d.bstride * 4);
     if (nbuf > bands) nbuf = bands;

@@ -3,26 +3,36 @@
 // Same integer result as the bit-parallel variant and as the reference's
 // cell recurrence (proj/src/serial.cpp:16-30, cell.hpp:20-38):
 //   c[i][j] = x_i == y_j ? c[i-1][j-1] + 1 : max(c[i-1][j], c[i][j-1])
-// evaluated branch-free with the Blackwell DPX three-way max as
-//   c = __vimax3_s32(up, left, diag + match)
-// (diag + match is one add-with-carry of the row's match bit)
-// (valid because c[i-1][j-1] + 1 >= max(up, left) on a match and
-// c[i-1][j-1] <= max(up, left) always).
 //
-// Tiling: a warp sweeps a band of 32*R rows (R consecutive rows per lane)
-// across all columns as an anti-diagonal wavefront -- lane l works on column
-// t - l at step t.  The bottom-row value of lane l-1 (the "up" of lane l's
-// first row) and the column byte travel down the warp in ONE packed
-// __shfl_up_sync per step ((value << 8) | byte); inside a lane the R rows
-// pass values in registers.  The match bits of a lane's R rows against a
-// column byte come from a per-lane 256-entry table in shared memory (one LDS
-// per step instead of R compares).  Band b+1 takes its top boundary from the
-// bottom row of band b.
+// Cells are packed two per 32-bit register (16x2) and updated with the DPX
+// SIMD three-way max, three ALU instructions per PAIR of cells:
+//   d = x ^ y                        (LOP3; per half 0 iff the codes match)
+//   t = diag + 0x00010001 - d        (IADD3; per half diag + 1 - d)
+//   c = vimax3_u16x2(up, left, t)    (VIMNMX3.U16x2)
+// On a match t = diag + 1, the reference's value; on a mismatch t <= diag,
+// and diag <= max(up, left) always, so t never wins.  The halves never borrow
+// from each other because every stored value is >= kOff > max d, and never
+// overflow because values are stored tile-relative (below).
 //
-//  * batch kernel: one warp per pair, bands processed in sequence by the same
-//    warp; the column string and the boundary row live in the warp's shared
-//    memory (column string = the shorter string, <= kWaveMaxCols bytes;
-//    longer pairs are listed for the single-pair kernel);
+// Tiling: a warp sweeps a band of 64 R rows as 64 "virtual lanes" of R
+// consecutive rows: lane l holds virtual lane l in the low halves of its
+// registers and virtual lane l + 32 in the high halves.  At step t lane l
+// works on column t - l (low) and t - l - 32 (high), so both halves are
+// independent cells -- an anti-diagonal wavefront 64 deep.  The bottom value
+// and the column code of each virtual lane travel to the next one in two
+// __shfl_sync per step; lane 0's high half takes lane 31's low half, lane 0's
+// low half takes the band's top boundary.  Columns before a virtual lane's
+// start carry a sentinel code that never matches, so no cell needs masking;
+// after the last column the state provably stops changing.
+//
+// Tile-relative values: stored = c - G with a warp-uniform base G (32-bit,
+// absolute values only on band borders).  The values one warp holds at a step
+// span at most ~64 R + 64, so the pair kernel re-bases every 8192 steps
+// (G += the warp's minimum - kOff) and the 16-bit halves never overflow.
+//
+//  * batch kernel: one warp per pair (columns = the shorter string <=
+//    kWaveMaxCols, in the warp's shared memory with the boundary row between
+//    bands); R chosen per pair so that the bands cover the rows tightly;
 //  * pair kernel: bands of one pair run concurrently on many warps; band b
 //    publishes its bottom row as self-validating words (value << 8 | tag)
 //    into a ring of boundary rows, band b+1 reads them in windows of 32
@@ -33,107 +43,183 @@
 namespace wlcs {
 namespace {
 
-constexpr int kWaveR = 8;           // rows per lane
-constexpr int kWaveBand = 32 * kWaveR;
-constexpr int kWaveWarps = 4;       // warps per CTA (batch kernel)
-constexpr int kWaveTab = 32 * 256;     // per-warp match table bytes: [lane][byte] -> R-bit row mask
+constexpr uint32_t kOff = 1024;           // stored value of c = 0 at the start
+constexpr uint32_t kOff2 = kOff * 0x10001u;
+constexpr uint32_t kSentinel = 0x100u;    // column code of no column
+constexpr uint32_t kNoRow = 0x1ffu;       // row code past the last row
+constexpr int kWaveWarps = 4;             // warps per CTA (batch kernel)
+constexpr int kRebaseMask = 8191;
+#ifndef WLCS_WAVE_SLEEP_NS
+#define WLCS_WAVE_SLEEP_NS 200
+#endif
+#ifndef WLCS_WAVE_PF_STEP
+#define WLCS_WAVE_PF_STEP 24
+#endif
+#ifndef WLCS_WAVE_MAX2
+#define WLCS_WAVE_MAX2 0
+#endif
 
+// One packed cell pair.  WLCS_WAVE_MAX2: the three-way max as two two-way
+// VIMNMX.16x2, which also issue on the FMA pipe (the ALU pipe keeps LOP3 and
+// IADD3); otherwise one VIMNMX3.U16x2 (ALU pipe only).  The second max is the
+// signed form so that ptxas does not fuse the pair back into VIMNMX3 (stored
+// values stay below 2^15: kOff + band + re-base period).
+__device__ __forceinline__ uint32_t cell2(uint32_t up, uint32_t left, uint32_t diag,
+                                          uint32_t x, uint32_t y) {
+    const uint32_t tt = diag + 0x10001u - (x ^ y);
+#if WLCS_WAVE_MAX2
+    const uint32_t q = __vmaxu2(left, tt);
+    uint32_t v;
+    asm("max.s16x2 %0, %1, %2;" : "=r"(v) : "r"(q), "r"(up));
+    return v;
+#else
+    return __vimax3_u16x2(up, left, tt);
+#endif
+}
 
-// Steps of one band: lane l owns rows i0 + R l + r and, at step t, the two
-// columns 2(t - l) and 2(t - l) + 1 (two columns per step halve the per-step
-// work of the shuffle, the bounds tests and the boundary hand-off).
-// Prov(t, upA, yA, upB, yB) is called by the whole warp at step t and sets,
-// for lane 0 (columns 2t, 2t+1), the top boundary c[i0-1][.] (0 for the first
-// band) and the column bytes; BottomFn(j, v) receives c[i0 + 32R - 1][j] from
-// lane 31.  Returns, in every lane, the final value of row `want_row` (0 if
-// not in this band).
-template <typename Prov, typename BottomFn>
+// Steps of one band, in windows of 32 steps.  Win(t0, G) is called by the
+// whole warp at the start of every window (the provider's hand-off waits and
+// conversions), Mid(t0) WLCS_WAVE_PF_STEP steps into it (the next window's
+// loads: late enough that the band above has usually written them, early
+// enough to land before they are needed); Prov(t) then returns, for lane 0 at step t, the
+// packed word (stored top boundary << 16) | code: the top boundary c[i0-1][t]
+// as c - G and the code of column t (kSentinel for t >= n, with a stored top
+// value in [kOff / 2, the last real one]).  Bottom(t, u, G) is called by
+// every lane at every step with its packed values u; lane 31's high half is
+// c[i0 + 64R - 1][t - 63] - G (meaningful for 0 <= t - 63 < n); the callee
+// stores it without a divergent branch (a branch around the store would put
+// the next step's shuffles on their slow path).  G changes only between
+// windows.  Returns, in every lane, the final value of row want_row (0 if not
+// in this band).
+template <int R, bool REBASE, typename Win, typename Mid, typename Prov, typename BottomFn>
 __device__ __forceinline__ int32_t sweep_band(const uint8_t* rowp, int64_t i0, int64_t m,
-                                              int64_t n, uint8_t* tab, Prov prov,
+                                              int64_t n, Win win, Mid mid, Prov prov,
                                               BottomFn bottom, int64_t want_row) {
     const int lane = int(lane_id());
-    // lane's match table: tab[lane][c] bit 7-r = (x_{i0 + R lane + r} == c)
-    uint8_t* mt = tab + lane * 256;
-    __syncwarp();
+    uint32_t xr[R];    // row codes: low half virtual lane `lane`, high half lane + 32
+    uint32_t left[R];  // current column's values of the R rows (both halves)
 #pragma unroll
-    for (int k = 0; k < 64; ++k) reinterpret_cast<uint32_t*>(mt)[k] = 0u;
-#pragma unroll
-    for (int r = 0; r < kWaveR; ++r) {
-        const int64_t i = i0 + int64_t(lane) * kWaveR + r;
-        if (i < m) mt[rowp[i]] |= uint8_t(0x80u >> r);  // row r at bit 7 - r
+    for (int r = 0; r < R; ++r) {
+        const int64_t ilo = i0 + int64_t(lane) * R + r, ihi = ilo + 32 * R;
+        const uint32_t lo = ilo < m ? uint32_t(rowp[ilo]) : kNoRow;
+        const uint32_t hi = ihi < m ? uint32_t(rowp[ihi]) : kNoRow;
+        xr[r] = lo | (hi << 16);
+        left[r] = kOff2;
     }
-    __syncwarp();
-    int32_t left[kWaveR];
+    int32_t G = -int32_t(kOff);  // c = stored + G
+    uint32_t prev_in = kOff2;     // up value of the previous column = diag of row 0
+    uint32_t send_v = kOff2, send_y = kSentinel * 0x10001u;
+    const int src = (lane + 31) & 31;
+    const int T = int(n) + 63;  // n < 2^24
+    auto step = [&](int t) {
+        const uint32_t rv = __shfl_sync(kFullMask, send_v, src);
+        const uint32_t ry = __shfl_sync(kFullMask, send_y, src);
+        const uint32_t pw = prov(t);
+        const uint32_t in_v = lane == 0 ? __byte_perm(pw, rv, 0x5432) : rv;
+        const uint32_t in_y = lane == 0 ? __byte_perm(pw, ry, 0x5410) : ry;
+        uint32_t u = in_v, dg = prev_in;
 #pragma unroll
-    for (int r = 0; r < kWaveR; ++r) left[r] = 0;
-    int32_t prev_up = 0;  // c[top-1][j-1] of this lane's first row
-    uint32_t sendA = 0, sendB = 0;
-    const int n2 = int((n + 1) >> 1);  // column pairs (n < 2^31)
-    const int T = n2 + 31;
-    // one column: 8 rows, each match bit shifted into the carry flag so that
-    // diag + match is one add-with-carry
-    auto column = [&](int32_t up, uint32_t y) {
-        uint32_t mm = uint32_t(mt[y]) << 24;
-        int32_t u = up, dg = prev_up;
-#pragma unroll
-        for (int r = 0; r < kWaveR; ++r) {
-            int32_t dm;
-            asm("{\n\tadd.cc.u32 %0, %0, %0;\n\taddc.u32 %1, %2, 0;\n\t}"
-                : "+r"(mm), "=r"(dm)
-                : "r"(dg));
-            const int32_t v = __vimax3_s32(u, left[r], dm);
+        for (int r = 0; r < R; ++r) {
+            const uint32_t v = cell2(u, left[r], dg, xr[r], in_y);
             dg = left[r];
             left[r] = v;
             u = v;
         }
-        prev_up = up;
-        return u;
+        prev_in = in_v;
+        send_v = u;
+        send_y = in_y;
+        bottom(t, u, G);
     };
-    for (int t = 0; t < T; ++t) {
-        const uint32_t ra = __shfl_up_sync(kFullMask, sendA, 1);
-        const uint32_t rb = __shfl_up_sync(kFullMask, sendB, 1);
-        const int jp = t - lane;  // column pair
-        int32_t upA0, upB0;
-        uint32_t yA0, yB0;
-        prov(t, upA0, yA0, upB0, yB0);
-        const int32_t upA = lane == 0 ? upA0 : int32_t(ra >> 8);
-        const uint32_t yA = lane == 0 ? yA0 : (ra & 0xffu);
-        const int32_t upB = lane == 0 ? upB0 : int32_t(rb >> 8);
-        const uint32_t yB = lane == 0 ? yB0 : (rb & 0xffu);
-        if (unsigned(jp) < unsigned(n2)) {
-            const int64_t ja = 2 * int64_t(jp);
-            const int32_t ua = column(upA, yA);
-            sendA = (uint32_t(ua) << 8) | yA;
-            if (lane == 31) bottom(ja, ua);
-            if (ja + 1 < n) {  // false only for the last pair of an odd n
-                const int32_t ub = column(upB, yB);
-                sendB = (uint32_t(ub) << 8) | yB;
-                if (lane == 31) bottom(ja + 1, ub);
+    if constexpr (!REBASE) {  // no windows (batch: Win is empty, G constant)
+        for (int t = 0; t < T; ++t) step(t);
+    } else {
+        for (int t0 = 0; t0 < T; t0 += 32) {
+            win(t0, G);
+            const int t1 = min(t0 + 32, T), tm = min(t0 + WLCS_WAVE_PF_STEP, t1);
+            for (int t = t0; t < tm; ++t) step(t);
+            mid(t0);
+            for (int t = tm; t < t1; ++t) step(t);
+            if (((t0 + 32) & kRebaseMask) == 0 && t0 + 32 <= int(n)) {
+                // row 0 of a virtual lane is its smallest value; the in-flight
+                // values (diag, sends, lane 0's top) are at most 2 below it.  Not
+                // in the last window: lane 0's past-the-end top values are a
+                // constant kOff / 2 that a re-base would wrap.
+                const uint32_t lmin = min(left[0] & 0xffffu, left[0] >> 16);
+                const uint32_t wmin = __reduce_min_sync(kFullMask, lmin);
+                if (wmin > 2 * kOff) {
+                    const uint32_t delta = wmin - kOff;
+                    const uint32_t d2 = delta * 0x10001u;
+#pragma unroll
+                    for (int r = 0; r < R; ++r) left[r] -= d2;
+                    prev_in -= d2;
+                    send_v -= d2;
+                    G += int32_t(delta);
+                }
             }
         }
     }
     int32_t res = 0;
     const int64_t k = want_row - i0;
-    if (k >= 0 && k < kWaveBand) {
-        const int owner = int(k / kWaveR), rr = int(k % kWaveR);
-        int32_t mine = left[0];
+    if (k >= 0 && k < 64 * R) {
+        const int vl = int(k / R), rr = int(k % R);
+        uint32_t mine = left[0];
 #pragma unroll
-        for (int r = 1; r < kWaveR; ++r)
+        for (int r = 1; r < R; ++r)
             if (r == rr) mine = left[r];
-        res = __shfl_sync(kFullMask, mine, owner);
+        const uint32_t w = __shfl_sync(kFullMask, mine, vl & 31);
+        res = int32_t(vl >= 32 ? (w >> 16) : (w & 0xffffu)) + G;
     }
     return res;
 }
 
+// Predicated shared store (no branch: see sweep_band).
+__device__ __forceinline__ void st_shared_u16_if(bool pred, uint16_t* p, uint32_t v) {
+    const uint32_t a = uint32_t(__cvta_generic_to_shared(p));
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %0, 0;\n\t"
+        "@p st.shared.u16 [%1], %2;\n\t}" ::"r"(uint32_t(pred)),
+        "r"(a), "h"(uint16_t(v)));
+}
+
 // ---------------------------------------------------------------- batch
+// Rows per virtual lane for a pair of m rows: the fewest bands of <= 64 * 16
+// rows, then the smallest even R >= 4 whose bands cover the rows.
+__device__ __forceinline__ int batch_rows_per_lane(int64_t m, int64_t& bands) {
+    bands = (m + 64 * 16 - 1) / (64 * 16);
+    const int64_t per = (m + bands - 1) / bands;
+    int R = int((per + 63) / 64);
+    R += R & 1;
+    return R < 4 ? 4 : R;
+}
+
+// A pair's columns live in the warp's shared memory as packed words
+// col[64 + j] = ((c[top][j] - G) << 16) | code(y_j), 64 words of padding on
+// both sides (sentinel code, c = 0): lane 0 reads its step's word without
+// bounds tests, and lane 31 writes the band's bottom row into the high halves
+// (column t - 63 at step t, i.e. word t + 1, already read by this band) for the
+// next band -- also without tests, the padding absorbs t - 63 < 0.
+template <int R>
+__device__ __forceinline__ int32_t batch_pair(const uint8_t* rowp, int64_t m, int64_t n,
+                                              uint32_t* col) {
+    int32_t res = 0;
+    uint16_t* col16 = reinterpret_cast<uint16_t*>(col);
+    const bool is31 = lane_id() == 31;
+    for (int64_t i0 = 0; i0 < m; i0 += 64 * R) {
+        const int32_t v = sweep_band<R, false>(
+            rowp, i0, m, n, [](int, int32_t) {}, [](int) {}, [&](int t) { return col[64 + t]; },
+            [&](int t, uint32_t u, int32_t) { st_shared_u16_if(is31, col16 + 2 * (t + 1) + 1, u >> 16); },
+            m - 1);
+        if (i0 + 64 * R >= m) res = v;
+        __syncwarp();
+    }
+    return res;
+}
+
 __global__ void __launch_bounds__(32 * kWaveWarps) wave_batch_kernel(WaveBatchDev d) {
-    extern __shared__ __align__(16) uint8_t smem[];
+    extern __shared__ __align__(16) uint32_t smem_w[];
     const int warp = int(threadIdx.x >> 5);
     const int lane = int(lane_id());
-    uint8_t* base = smem + warp * (kWaveMaxCols * 5 + kWaveTab);
-    int32_t* bnd = reinterpret_cast<int32_t*>(base);
-    uint8_t* cs = base + kWaveMaxCols * 4;
-    uint8_t* tab = base + kWaveMaxCols * 5;
+    uint32_t* col = smem_w + warp * (kWaveMaxCols + 128);
     for (;;) {
         uint32_t p = 0;
         if (lane == 0) p = atomicAdd(d.counter, 1u);
@@ -155,24 +241,22 @@ __global__ void __launch_bounds__(32 * kWaveWarps) wave_batch_kernel(WaveBatchDe
             continue;
         }
         __syncwarp();
-        for (int64_t k = lane; k < n; k += 32) cs[k] = colp[k];
+        for (int k = lane; k < int(n) + 128; k += 32) {
+            const int j = k - 64;
+            col[k] = (kOff << 16) | ((j >= 0 && j < n) ? uint32_t(colp[j]) : kSentinel);
+        }
         __syncwarp();
-        int32_t res = 0;
-        for (int64_t i0 = 0; i0 < m; i0 += kWaveBand) {
-            const bool first = i0 == 0;
-            const int32_t v = sweep_band(
-                rowp, i0, m, n, tab,
-                [&](int t, int32_t& upA, uint32_t& yA, int32_t& upB, uint32_t& yB) {
-                    const int64_t ja = 2 * int64_t(t);
-                    const bool ina = lane == 0 && ja < n, inb = lane == 0 && ja + 1 < n;
-                    upA = (ina && !first) ? bnd[ja] : 0;
-                    yA = ina ? uint32_t(cs[ja]) : 0u;
-                    upB = (inb && !first) ? bnd[ja + 1] : 0;
-                    yB = inb ? uint32_t(cs[ja + 1]) : 0u;
-                },
-                [&](int64_t j, int32_t v) { bnd[j] = v; }, m - 1);
-            if (i0 + kWaveBand >= m) res = v;
-            __syncwarp();
+        int64_t bands;
+        const int R = batch_rows_per_lane(m, bands);
+        int32_t res;
+        switch (R) {
+            case 4: res = batch_pair<4>(rowp, m, n, col); break;
+            case 6: res = batch_pair<6>(rowp, m, n, col); break;
+            case 8: res = batch_pair<8>(rowp, m, n, col); break;
+            case 10: res = batch_pair<10>(rowp, m, n, col); break;
+            case 12: res = batch_pair<12>(rowp, m, n, col); break;
+            case 14: res = batch_pair<14>(rowp, m, n, col); break;
+            default: res = batch_pair<16>(rowp, m, n, col); break;
         }
         if (lane == 0) d.out[p] = uint32_t(res);
     }
@@ -184,67 +268,76 @@ __device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
     asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
-__device__ __forceinline__ void st_relaxed(uint32_t* p, uint32_t v) {
-    asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+__device__ __forceinline__ void st_relaxed_if(bool pred, uint32_t* p, uint32_t v) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %0, 0;\n\t"
+        "@p st.relaxed.gpu.global.u32 [%1], %2;\n\t}" ::"r"(uint32_t(pred)),
+        "l"(p), "r"(v)
+        : "memory");
 }
 
+template <int R>
 __global__ void __launch_bounds__(32) wave_pair_kernel(WavePairDev d) {
-    __shared__ __align__(16) uint8_t tab[kWaveTab];
     const int lane = int(lane_id());
     const int64_t n = d.n, m = d.m;
-    const uint32_t nbands = uint32_t((m + kWaveBand - 1) / kWaveBand);
+    constexpr int kBand = 64 * R;
+    const uint32_t nbands = uint32_t((m + kBand - 1) / kBand);
     for (;;) {
         uint32_t b = 0;
         if (lane == 0) b = atomicAdd(d.ticket, 1u);
         b = __shfl_sync(kFullMask, b, 0);
         if (b >= nbands) break;
-        const int64_t i0 = int64_t(b) * kWaveBand;
+        const int64_t i0 = int64_t(b) * kBand;
         const bool first = b == 0, last = b + 1 == nbands;
         // ring of nbuf boundary rows; words are (value << 8) | tag with the
         // writer's generation tag, so stale words of an earlier band are
         // recognised without re-zeroing (a band b+nbuf-1 that reuses band b-1's
         // row writes column j only after band b has read it: band b+k reaches
-        // column j no earlier than 31 k steps after band b)
+        // column j no earlier than 64 k steps after band b)
         const uint32_t prev_tag = first ? 0u : ((b - 1) / d.nbuf) % 255u + 1u;
         const uint32_t my_tag = (b / d.nbuf) % 255u + 1u;
         const uint32_t* above = d.bnd + int64_t(first ? 0 : (b - 1) % d.nbuf) * d.bstride;
         uint32_t* below = d.bnd + int64_t(b % d.nbuf) * d.bstride;
-        // windows of 32 columns: lane k holds column base + k (boundary word
-        // and column byte) for the current and the next window
+        // windows of 32 columns: lane k loads column base + k (boundary word
+        // and column byte) of the next window during the current one; at a
+        // window's start they become lane 0's packed provider words for its
+        // 32 steps
         auto load_win = [&](int64_t base, uint32_t& w, uint32_t& c) {
             const int64_t jj = base + lane;
             w = (!first && jj < n) ? ld_relaxed(above + jj) : prev_tag;
-            c = jj < n ? uint32_t(d.colp[jj]) : 0u;
+            c = jj < n ? uint32_t(d.colp[jj]) : kSentinel;
         };
-        uint32_t cw, cc, nw, nc;
-        load_win(0, cw, cc);
-        load_win(32, nw, nc);
-        const int32_t v = sweep_band(
-            d.rowp, i0, m, n, tab,
-            [&](int t, int32_t& upA, uint32_t& yA, int32_t& upB, uint32_t& yB) {
-                const int64_t ja = 2 * int64_t(t);  // columns ja, ja + 1 (same window)
-                if ((ja & 31) == 0 && ja < n) {
-                    if (ja > 0) {
-                        cw = nw;
-                        cc = nc;
-                        load_win(ja + 32, nw, nc);
-                    }
-                    // wait until band b-1 has published the whole window
-                    while (__any_sync(kFullMask, (cw & 0xffu) != prev_tag))
-                        if ((cw & 0xffu) != prev_tag) cw = ld_relaxed(above + ja + lane);
+        uint32_t nw, nc, pwin = 0;
+        load_win(0, nw, nc);
+        const int ni = int(n);
+        const int32_t v = sweep_band<R, true>(
+            d.rowp, i0, m, n,
+            [&](int t0, int32_t G) {
+                if (t0 >= ni) {
+                    pwin = ((kOff / 2) << 16) | kSentinel;
+                    return;
                 }
-                const int la = int(ja & 31);
-                const uint32_t wa = __shfl_sync(kFullMask, cw, la);
-                const uint32_t ca = __shfl_sync(kFullMask, cc, la);
-                const uint32_t wb = __shfl_sync(kFullMask, cw, la + 1);
-                const uint32_t cb = __shfl_sync(kFullMask, cc, la + 1);
-                upA = (first || ja >= n) ? 0 : int32_t(wa >> 8);
-                yA = ca;
-                upB = (first || ja + 1 >= n) ? 0 : int32_t(wb >> 8);
-                yB = cb;
+                uint32_t cw = nw;
+                const uint32_t cc = nc;
+                // wait until band b-1 has published the whole window; a
+                // waiting warp sleeps between polls so that it does not take
+                // issue slots from the warps that compute
+                while (__any_sync(kFullMask, (cw & 0xffu) != prev_tag)) {
+                    __nanosleep(WLCS_WAVE_SLEEP_NS);
+                    if ((cw & 0xffu) != prev_tag) cw = ld_relaxed(above + t0 + lane);
+                }
+                const int32_t top = first ? 0 : int32_t(cw >> 8);
+                pwin = t0 + lane < ni ? (uint32_t(top - G) << 16) | cc
+                                      : ((kOff / 2) << 16) | kSentinel;
             },
-            [&](int64_t j, int32_t val) {
-                if (!last) st_relaxed(below + j, (uint32_t(val) << 8) | my_tag);
+            [&](int t0) {
+                if (t0 + 32 < ni) load_win(t0 + 32, nw, nc);
+            },
+            [&](int t) { return __shfl_sync(kFullMask, pwin, t & 31); },
+            [&](int t, uint32_t u, int32_t G) {
+                const int jb = t - 63;
+                st_relaxed_if(lane == 31 && !last && jb >= 0, below + jb,
+                              (uint32_t(int32_t(u >> 16) + G) << 8) | my_tag);
             },
             m - 1);
         if (last && lane == 0) *d.out = uint32_t(v);
@@ -253,7 +346,7 @@ __global__ void __launch_bounds__(32) wave_pair_kernel(WavePairDev d) {
 
 }  // namespace
 
-size_t wave_batch_smem() { return size_t(kWaveWarps) * (kWaveMaxCols * 5 + kWaveTab); }
+size_t wave_batch_smem() { return size_t(kWaveWarps) * (kWaveMaxCols + 128) * 4; }
 
 cudaError_t wave_batch_launch(const WaveBatchDev& d, int sms, cudaStream_t stream) {
     const int smem = int(wave_batch_smem());
@@ -273,18 +366,37 @@ cudaError_t wave_batch_launch(const WaveBatchDev& d, int sms, cudaStream_t strea
     return cudaGetLastError();
 }
 
-int64_t wave_pair_bands(int64_t m) { return (m + kWaveBand - 1) / kWaveBand; }
+// Rows per virtual lane: the tallest bands (least hand-off and pipeline
+// fill) that still give every SM about 12 resident warps.
+int wave_pair_rows(int64_t m, int sms) {
+    for (int R : {16, 8})
+        if ((m + 64 * R - 1) / (64 * R) >= int64_t(sms) * 12) return R;
+    return 4;
+}
 
-cudaError_t wave_pair_launch(const WavePairDev& d, int sms, cudaStream_t stream) {
+int64_t wave_pair_bands(int64_t m, int R) { return (m + 64 * R - 1) / (64 * R); }
+
+template <int R>
+cudaError_t wave_pair_launch_r(const WavePairDev& d, int sms, cudaStream_t stream) {
     int occ = 0;
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, wave_pair_kernel, 32, 0);
+    cudaError_t e =
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, wave_pair_kernel<R>, 32, 0);
     if (e != cudaSuccess) return e;
     if (occ < 1) occ = 1;
-    int64_t grid = int64_t(sms) * (occ < 8 ? occ : 8);
-    const int64_t bands = wave_pair_bands(d.m);
+    int64_t grid = int64_t(sms) * (occ < 16 ? occ : 16);
+    const int64_t bands = wave_pair_bands(d.m, R);
     if (grid > bands) grid = bands;
-    wave_pair_kernel<<<int(grid), 32, 0, stream>>>(d);
+    wave_pair_kernel<R><<<int(grid), 32, 0, stream>>>(d);
     return cudaGetLastError();
+}
+
+cudaError_t wave_pair_launch(const WavePairDev& d, int sms, cudaStream_t stream) {
+    switch (d.R) {
+        case 16: return wave_pair_launch_r<16>(d, sms, stream);
+        case 8: return wave_pair_launch_r<8>(d, sms, stream);
+        case 4: return wave_pair_launch_r<4>(d, sms, stream);
+        default: return cudaErrorInvalidValue;
+    }
 }
 
 }  // namespace wlcs

@@ -159,7 +159,7 @@ cudaError_t pair_walk(const PairDev& d, int K, const uint8_t* x, uint8_t* out,
 namespace wlcs {
 
 // ---- cell-wavefront variant (wavefront.cu) ----
-constexpr int kWaveMaxCols = 4096;  // batch kernel: shorter string per pair
+constexpr int kWaveMaxCols = 2048;  // batch kernel: shorter string per pair
 
 struct WaveBatchDev {
     const uint8_t* xs;
@@ -183,6 +183,7 @@ struct WavePairDev {
     uint32_t nbuf;        // >= 2
     uint32_t* ticket;     // band ticket (zeroed)
     uint32_t* out;        // LCS length
+    int R;                // rows per virtual lane (wave_pair_rows): bands of 64 R rows
 };
 
 // ---- the reference's block-kernel contract on the device (tiles.cu) ----
@@ -194,7 +195,8 @@ cudaError_t tile_fill(const uint8_t* d_x, const uint8_t* d_y, const uint32_t* d_
 
 size_t wave_batch_smem();
 cudaError_t wave_batch_launch(const WaveBatchDev& d, int sms, cudaStream_t stream);
-int64_t wave_pair_bands(int64_t m);
+int wave_pair_rows(int64_t m, int sms);
+int64_t wave_pair_bands(int64_t m, int R);
 cudaError_t wave_pair_launch(const WavePairDev& d, int sms, cudaStream_t stream);
 
 }  // namespace wlcs

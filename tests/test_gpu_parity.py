@@ -300,14 +300,25 @@ def test_wavefront_batch_edges(wl, restatement):
 
 
 @pytest.mark.parametrize("m,n", [(1, 1), (127, 129), (129, 127), (1000, 1000), (4096, 33),
-                                 (5000, 200), (20000, 7000)])
+                                 (5000, 200), (20000, 7000), (150000, 70000)])
 def test_wavefront_pair(wl, restatement, m, n):
     rng = np.random.default_rng(m * 7 + n)
     x = rng.choice(np.frombuffer(DNA, np.uint8), m).tobytes()
     y = rng.choice(np.frombuffer(DNA, np.uint8), n).tobytes()
     want = restatement.length_bitpar(x, y)
-    assert wl.lcs_length(x, y, variant=wl.VARIANT_WAVEFRONT) == want
-    assert wl.lcs_length(x, y, variant=wl.VARIANT_BITPARALLEL) == want
+    assert wl.lcs_length(x, y, wl.NO_BUDGET, variant=wl.VARIANT_WAVEFRONT) == want
+    assert wl.lcs_length(x, y, wl.NO_BUDGET, variant=wl.VARIANT_BITPARALLEL) == want
+
+
+def test_wavefront_pair_rebase(wl, restatement):
+    """Identical strings: the LCS grows by one per column, so the 16-bit
+    packed values must be re-based (every 8192 steps) well before 2^16."""
+    rng = np.random.default_rng(77)
+    x = rng.choice(np.frombuffer(DNA, np.uint8), 100_000).tobytes()
+    assert wl.lcs_length(x, x, wl.NO_BUDGET, variant=wl.VARIANT_WAVEFRONT) == 100_000
+    y = x[:60_000] + b"T" * 20_000 + x[60_000:90_000]  # 110,000 columns
+    assert wl.lcs_length(x, y, wl.NO_BUDGET, variant=wl.VARIANT_WAVEFRONT) == \
+        restatement.length_bitpar(x, y)
 
 
 def test_wavefront_c1_checkpoint(wl):
