@@ -242,6 +242,18 @@ int wlcs_length_strips(const uint8_t* x, size_t m, const uint8_t* y, size_t n, i
 int wlcs_colsplit_emulate(const uint8_t* x, size_t m, const uint8_t* y, size_t n, int slices,
                           int max_ctas, uint32_t* out);
 
+/* Row-band decomposition of one pair (prototype): the
+ * rows of x are cut into `bands` equal bands that are combed INDEPENDENTLY
+ * (semi-local LCS, seaweed combing; one warp per band, all bands in one
+ * launch) and composed top to bottom through their DP boundaries
+ * (C[j] = max_{i<=j} T[i] + H(i, j), exact).  The route to splitting a long
+ * pair's rows across GPUs; today a correctness prototype (cell-level combing,
+ * O(n^2) combine), not the fast path.  Replaces no reference entry point: the
+ * reference's only schedule is the row-serial wavefront
+ * (proj/src/parallel.cpp:172-226).  *out = LCS length. */
+int wlcs_length_rowbands(const uint8_t* x, size_t m, const uint8_t* y, size_t n, int bands,
+                         uint32_t* out);
+
 /* Device memory helpers for the inboxes (current device). */
 int wlcs_device_alloc(size_t bytes, void** d_ptr); /* zero-filled */
 int wlcs_device_zero(void* d_ptr, size_t bytes);

@@ -124,6 +124,7 @@ lib.wlcs_ipc_open.argtypes = [ctypes.c_char_p, ctypes.POINTER(ctypes.c_void_p)]
 lib.wlcs_ipc_close.argtypes = [_vp]
 lib.wlcs_fill_tables.argtypes = [_vp, _sz, _vp, _sz, _sz, _vp, _vp]
 lib.wlcs_colsplit_emulate.argtypes = [_vp, _sz, _vp, _sz, ctypes.c_int, ctypes.c_int, _u32p]
+lib.wlcs_length_rowbands.argtypes = [_vp, _sz, _vp, _sz, ctypes.c_int, _u32p]
 lib.wlcs_length_batch_multi.argtypes = [_vp, _u64p, _vp, _u64p, _sz, ctypes.c_int,
                                         ctypes.POINTER(ctypes.c_uint32)]
 lib.wlcs_length_strips.argtypes = [_vp, _sz, _vp, _sz, ctypes.c_int,
@@ -316,6 +317,16 @@ def colsplit_emulate(x, y, slices: int, max_ctas: int = 0) -> int:
     out = ctypes.c_uint32()
     _check(lib.wlcs_colsplit_emulate(xb, len(xb), yb, len(yb), slices, max_ctas,
                                      ctypes.byref(out)))
+    return int(out.value)
+
+
+def lcs_length_rowbands(x, y, bands: int) -> int:
+    """LCS length with the rows of x cut into `bands` bands that are combed
+    independently (semi-local LCS) and composed exactly (prototype of the
+    row split; csrc/seaweed.cu)."""
+    xb, yb = _as_bytes(x), _as_bytes(y)
+    out = ctypes.c_uint32()
+    _check(lib.wlcs_length_rowbands(xb, len(xb), yb, len(yb), bands, ctypes.byref(out)))
     return int(out.value)
 
 

@@ -97,7 +97,7 @@ struct Ctx {
     // batch (ws: first pass per chunk; ws2 + wcarry: the device second pass)
     DevBuf xs, ys, xoff, yoff, out, ws, ws2, wcarry;
     // single pair
-    DevBuf px, py, pmg, carry, small, rows, outrev, codes, ry, vbuf, wave, sink, walk, tile;
+    DevBuf px, py, pmg, carry, small, rows, outrev, codes, ry, vbuf, wave, sink, walk, tile, sea;
     DevBuf ckpt, bandcodes;  // banded traceback
     ~Ctx() {
         if (hscratch) cudaFreeHost(hscratch);
@@ -1140,6 +1140,53 @@ int wlcs_length_ex(const uint8_t* x, size_t m, const uint8_t* y, size_t n, size_
 int wlcs_length(const uint8_t* x, size_t m, const uint8_t* y, size_t n, size_t memory_budget,
                 uint32_t* out) {
     return wlcs_length_ex(x, m, y, n, memory_budget, WLCS_VARIANT_BITPARALLEL, out);
+}
+
+// Row-band decomposition (seaweed.cu): the rows of x in `bands` equal bands,
+// each combed independently, composed through their DP boundaries.
+int wlcs_length_rowbands(const uint8_t* x, size_t m, const uint8_t* y, size_t n, int bands,
+                         uint32_t* out) {
+    if (!out) return fail(WLCS_E_INVALID_ARGUMENT, "out is NULL");
+    if ((m && !x) || (n && !y)) return fail(WLCS_E_INVALID_ARGUMENT, "NULL input");
+    if (bands < 1) return fail(WLCS_E_INVALID_ARGUMENT, "bands must be >= 1");
+    if (m == 0 || n == 0) {
+        *out = 0;
+        return WLCS_OK;
+    }
+    if (n >= (size_t(1) << 31) || m >= (size_t(1) << 31))
+        return fail(WLCS_E_CONFIG, "row-band prototype: strings must be < 2^31 bytes");
+    if (size_t(bands) > m) bands = int(m);
+    Ctx* c = nullptr;
+    int rc = get_ctx(&c);
+    if (rc) return rc;
+    WLCS_CUDA(c->px.ensure(m + 16));
+    WLCS_CUDA(c->py.ensure(n + 16));
+    if (int rc_ = h2d_staged(*c, c->px.p, x, m, c->stream)) return rc_;
+    if (int rc_ = h2d_staged(*c, c->py.p, y, n, c->stream)) return rc_;
+    // [row_lo: bands + 1 int64][out][v: bands * n][e: bands * n][t0, t1: n + 1]
+    const size_t lo_bytes = (size_t(bands) + 1) * 8 + 16;
+    const size_t vb = size_t(bands) * n * 4;
+    WLCS_CUDA(c->sea.ensure(lo_bytes + 2 * vb + 2 * (n + 1) * 4 + 64));
+    uint8_t* base = c->sea.as<uint8_t>();
+    std::vector<int64_t> lo(size_t(bands) + 1);
+    for (int b = 0; b <= bands; ++b) lo[size_t(b)] = int64_t(m * size_t(b) / size_t(bands));
+    WLCS_CUDA(cudaMemcpyAsync(base, lo.data(), lo.size() * 8, cudaMemcpyHostToDevice, c->stream));
+    uint32_t* d_out = reinterpret_cast<uint32_t*>(base + lo_bytes - 16);
+    wlcs::SeaDev d{};
+    d.rowp = c->px.as<uint8_t>();
+    d.row_lo = reinterpret_cast<const int64_t*>(base);
+    d.colp = c->py.as<uint8_t>();
+    d.n = int64_t(n);
+    d.v = reinterpret_cast<uint32_t*>(base + lo_bytes);
+    d.e = d.v + size_t(bands) * n;
+    uint32_t* t0 = d.e + size_t(bands) * n;
+    uint32_t* t1 = t0 + (n + 1);
+    WLCS_CUDA(wlcs::seaweed_bands(d, bands, t0, t1, d_out, c->stream));
+    uint32_t* h = reinterpret_cast<uint32_t*>(c->hscratch);
+    WLCS_CUDA(cudaMemcpyAsync(h, d_out, 4, cudaMemcpyDeviceToHost, c->stream));
+    WLCS_CUDA(stream_wait(c->stream));
+    *out = *h;
+    return WLCS_OK;
 }
 
 int wlcs_length_device(const uint8_t* d_x, size_t m, const uint8_t* d_y, size_t n, int variant,

@@ -186,6 +186,21 @@ struct WavePairDev {
     int R;                // rows per virtual lane (wave_pair_rows): bands of 64 R rows
 };
 
+// ---- row-band decomposition through seaweed combing (seaweed.cu) ----
+struct SeaDev {
+    const uint8_t* rowp;    // rows (m bytes)
+    const int64_t* row_lo;  // [bands + 1] band row bounds (device)
+    const uint8_t* colp;    // columns (n bytes)
+    int64_t n;
+    uint32_t* v;            // [bands][n] column seaweeds (scratch)
+    uint32_t* e;            // [bands][n] exit column of each top seaweed (n = right side)
+};
+// Combs every band (one launch, bands concurrent), then composes the bands
+// top to bottom through their DP boundaries; *out (device) = the length.
+// t0, t1: n + 1 words each.
+cudaError_t seaweed_bands(const SeaDev& d, int bands, uint32_t* t0, uint32_t* t1,
+                          uint32_t* out, cudaStream_t stream);
+
 // ---- the reference's block-kernel contract on the device (tiles.cu) ----
 // Tile of h x w cells from its north row (w + 1 values, corner first) and
 // west column (h values); cv / bv receive the tile's cells and arrows.

@@ -321,6 +321,31 @@ def test_wavefront_pair_rebase(wl, restatement):
         restatement.length_bitpar(x, y)
 
 
+# ---- row-band decomposition (semi-local LCS prototype, csrc/seaweed.cu) ----
+
+@pytest.mark.parametrize("bands", [1, 2, 3, 4])
+@pytest.mark.parametrize("alphabet", [DNA, PROTEIN, bytes(range(256))])
+def test_rowbands_random(wl, restatement, bands, alphabet):
+    rng = np.random.default_rng(bands * 31 + len(alphabet))
+    al = np.frombuffer(alphabet, np.uint8)
+    for m, n in [(1, 1), (1, 40), (40, 1), (255, 257), (700, 300), (300, 700), (2500, 1900)]:
+        x = rng.choice(al, m).tobytes()
+        y = rng.choice(al, n).tobytes()
+        assert wl.lcs_length_rowbands(x, y, bands) == restatement.length_bitpar(x, y), (m, n)
+
+
+def test_rowbands_edges(wl, restatement):
+    assert wl.lcs_length_rowbands(b"", b"ACGT", 3) == 0
+    assert wl.lcs_length_rowbands(b"ACGT", b"", 3) == 0
+    assert wl.lcs_length_rowbands(b"ACGT", b"ACGT", 9) == 4  # more bands than rows
+    x = b"A" * 3000
+    assert wl.lcs_length_rowbands(x, x, 4) == 3000          # identical strings
+    assert wl.lcs_length_rowbands(x, b"C" * 2000, 4) == 0   # no match at all
+    from paper_1306_4627_b200 import workloads
+    x, y = workloads.config_pair("c1")                        # 10k x 10k
+    assert wl.lcs_length_rowbands(x, y, 4) == 6538
+
+
 def test_wavefront_c1_checkpoint(wl):
     from paper_1306_4627_b200 import workloads
     x, y = workloads.config_pair("c1")
