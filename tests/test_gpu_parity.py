@@ -621,10 +621,10 @@ def test_batch_device_is_ordered_on_caller_stream(wl, restatement):
     with torch.cuda.stream(side):
         d_xs = torch.zeros(len(xb) + 16, dtype=torch.uint8, device=dev)
         d_ys = torch.zeros(len(yb) + 16, dtype=torch.uint8, device=dev)
-        d_xs[: len(xb)].copy_(torch.from_numpy(xb), non_blocking=False)
-        d_ys[: len(yb)].copy_(torch.from_numpy(yb), non_blocking=False)
-        d_xo = torch.from_numpy(xo.view(np.int64)).to(dev)
-        d_yo = torch.from_numpy(yo.view(np.int64)).to(dev)
+        d_xs[: len(xb)].copy_(torch.from_numpy(np.array(xb)), non_blocking=False)
+        d_ys[: len(yb)].copy_(torch.from_numpy(np.array(yb)), non_blocking=False)
+        d_xo = torch.from_numpy(np.array(xo.view(np.int64))).to(dev)
+        d_yo = torch.from_numpy(np.array(yo.view(np.int64))).to(dev)
         d_out = torch.full((len(xs),), -1, dtype=torch.int32, device=dev)
         wl.lcs_length_batch_device(d_xs.data_ptr(), d_xo.data_ptr(), d_ys.data_ptr(),
                                    d_yo.data_ptr(), len(xs), len(xb), len(yb), d_out.data_ptr(),
