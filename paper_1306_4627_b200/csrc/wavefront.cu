@@ -183,12 +183,16 @@ __device__ __forceinline__ void st_shared_u16_if(bool pred, uint16_t* p, uint32_
 
 // ---------------------------------------------------------------- batch
 // Rows per virtual lane for a pair of m rows: the fewest bands of <= 64 * 16
-// rows, then the smallest even R >= 4 whose bands cover the rows.
+// rows, then the smallest R >= 4 whose bands cover the rows (odd R too unless
+// WLCS_WAVE_EVEN_R: at most 63 padding rows per band).
+#ifndef WLCS_WAVE_EVEN_R
+#define WLCS_WAVE_EVEN_R 0
+#endif
 __device__ __forceinline__ int batch_rows_per_lane(int64_t m, int64_t& bands) {
     bands = (m + 64 * 16 - 1) / (64 * 16);
     const int64_t per = (m + bands - 1) / bands;
     int R = int((per + 63) / 64);
-    R += R & 1;
+    if (WLCS_WAVE_EVEN_R) R += R & 1;
     return R < 4 ? 4 : R;
 }
 
@@ -251,11 +255,17 @@ __global__ void __launch_bounds__(32 * kWaveWarps) wave_batch_kernel(WaveBatchDe
         int32_t res;
         switch (R) {
             case 4: res = batch_pair<4>(rowp, m, n, col); break;
+            case 5: res = batch_pair<5>(rowp, m, n, col); break;
             case 6: res = batch_pair<6>(rowp, m, n, col); break;
+            case 7: res = batch_pair<7>(rowp, m, n, col); break;
             case 8: res = batch_pair<8>(rowp, m, n, col); break;
+            case 9: res = batch_pair<9>(rowp, m, n, col); break;
             case 10: res = batch_pair<10>(rowp, m, n, col); break;
+            case 11: res = batch_pair<11>(rowp, m, n, col); break;
             case 12: res = batch_pair<12>(rowp, m, n, col); break;
+            case 13: res = batch_pair<13>(rowp, m, n, col); break;
             case 14: res = batch_pair<14>(rowp, m, n, col); break;
+            case 15: res = batch_pair<15>(rowp, m, n, col); break;
             default: res = batch_pair<16>(rowp, m, n, col); break;
         }
         if (lane == 0) d.out[p] = uint32_t(res);
