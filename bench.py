@@ -579,7 +579,9 @@ def single_pair_block(name, steps, warmup, dist, peak_ops):
             "roofline": {"bound": "int", "achieved": round(achieved, 3),
                          "peak": round(peak_ops / 1e12, 3), "unit": "Tops/s",
                          "frac": round(achieved / (peak_ops / 1e12), 4),
-                         "kernel": "pair_strip_kernel"},
+                         "kernel": "pair_strip_kernel",
+                         "traffic": ncu_traffic(f"pair_strip_kernel_{name}"),
+                         "algorithmic_bytes": len(x) + len(y)},
             "steps": steps}
 
 
