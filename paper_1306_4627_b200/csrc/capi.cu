@@ -348,7 +348,8 @@ int watchdog_failed(Ctx& c) {
     const uint32_t err = uint32_t(c.hscratch[7]);
     if (err == 0) return WLCS_OK;
     return fail(WLCS_E_INTERNAL,
-                "strip kernel: carry words of a neighbouring slice never arrived (watchdog)");
+                "fill kernel: a hand-off word of a neighbouring strip / band / slice never "
+                "arrived (watchdog)");
 }
 
 int pair_setup(Ctx& c, const uint8_t* d_row, int64_t rows, const uint8_t* d_col, int64_t cols,
@@ -501,8 +502,9 @@ int pair_wave_device(Ctx& c, const uint8_t* dx, size_t m, const uint8_t* dy, siz
     d.bnd = c.wave.as<uint32_t>();
     d.ticket = reinterpret_cast<uint32_t*>(c.small.as<uint8_t>() + 1600);
     d.out = d.ticket + 1;
+    d.error = reinterpret_cast<uint32_t*>(c.small.as<uint8_t>() + kErrOff);
     WLCS_CUDA(cudaMemsetAsync(d.bnd, 0, bytes, c.stream));
-    WLCS_CUDA(cudaMemsetAsync(d.ticket, 0, 8, c.stream));
+    WLCS_CUDA(cudaMemsetAsync(d.error, 0, 1608 - kErrOff, c.stream));  // error, ticket, out
     if (c.timing && !c.ev0) {
         WLCS_CUDA(cudaEventCreate(&c.ev0));
         WLCS_CUDA(cudaEventCreate(&c.ev1));
@@ -511,12 +513,13 @@ int pair_wave_device(Ctx& c, const uint8_t* dx, size_t m, const uint8_t* dy, siz
     WLCS_CUDA(wlcs::wave_pair_launch(d, c.sms, c.stream));
     if (c.timing) WLCS_CUDA(cudaEventRecord(c.ev1, c.stream));
     WLCS_CUDA(cudaMemcpyAsync(out, d.out, 4, cudaMemcpyDeviceToHost, c.stream));
+    if (int rc = watchdog_read(c, c.stream)) return rc;
     WLCS_CUDA(stream_wait(c.stream));
     if (c.timing) {
         WLCS_CUDA(cudaEventElapsedTime(&c.last_main_ms, c.ev0, c.ev1));
         c.timing_pending = false;
     }
-    return WLCS_OK;
+    return watchdog_failed(c);
 }
 
 int pair_length_variant(Ctx& c, const uint8_t* dx, size_t m, const uint8_t* dy, size_t n,

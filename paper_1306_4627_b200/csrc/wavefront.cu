@@ -318,6 +318,7 @@ __global__ void __launch_bounds__(32) wave_pair_kernel(WavePairDev d) {
             c = jj < n ? uint32_t(d.colp[jj]) : kSentinel;
         };
         uint32_t nw, nc, pwin = 0;
+        bool failed = false;  // warp-uniform: set by the watchdog
         load_win(0, nw, nc);
         const int ni = int(n);
         const int32_t v = sweep_band<R, true>(
@@ -332,9 +333,15 @@ __global__ void __launch_bounds__(32) wave_pair_kernel(WavePairDev d) {
                 // wait until band b-1 has published the whole window; a
                 // waiting warp sleeps between polls so that it does not take
                 // issue slots from the warps that compute
+                uint32_t spins = 0;
                 while (__any_sync(kFullMask, (cw & 0xffu) != prev_tag)) {
                     __nanosleep(WLCS_WAVE_SLEEP_NS);
                     if ((cw & 0xffu) != prev_tag) cw = ld_relaxed(above + t0 + lane);
+                    if (++spins > (1u << 24)) {  // watchdog (~1 min): fail, do not hang
+                        if (lane == 0) atomicOr(d.error, 1u);
+                        failed = true;
+                        break;
+                    }
                 }
                 const int32_t top = first ? 0 : int32_t(cw >> 8);
                 pwin = t0 + lane < ni ? (uint32_t(top - G) << 16) | cc
@@ -350,6 +357,7 @@ __global__ void __launch_bounds__(32) wave_pair_kernel(WavePairDev d) {
                               (uint32_t(int32_t(u >> 16) + G) << 8) | my_tag);
             },
             m - 1);
+        if (failed) return;  // the error word is set; the host reports it
         if (last && lane == 0) *d.out = uint32_t(v);
     }
 }

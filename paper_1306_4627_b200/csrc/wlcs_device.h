@@ -183,6 +183,7 @@ struct WavePairDev {
     uint32_t nbuf;        // >= 2
     uint32_t* ticket;     // band ticket (zeroed)
     uint32_t* out;        // LCS length
+    uint32_t* error;      // watchdog flag (zeroed): a hand-off word never arrived
     int R;                // rows per virtual lane (wave_pair_rows): bands of 64 R rows
 };
 
