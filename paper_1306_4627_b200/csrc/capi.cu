@@ -664,8 +664,18 @@ int batch_pipe_copies(Ctx& c, const uint8_t* xs, const uint64_t* x_off, const ui
         c.chunk_ev.push_back(e);
     }
     const int pm_bytes = batch_pm_bytes();
+    // tapered chunks (weights nchunks, nchunks - 1, ..., 1): the compute of
+    // each chunk hides under the next chunk's copy either way, and the last
+    // chunk -- whose compute is the exposed tail after the final copy -- is
+    // the smallest (WLCS_BATCH_TAPER=0: equal chunks)
     pp.p0.assign(nchunks + 1, 0);
-    for (int k = 0; k <= nchunks; ++k) pp.p0[k] = pairs * size_t(k) / size_t(nchunks);
+    const bool taper = env_int("WLCS_BATCH_TAPER", 1) != 0;
+    const size_t wsum = taper ? size_t(nchunks) * size_t(nchunks + 1) / 2 : size_t(nchunks);
+    size_t wacc = 0;
+    for (int k = 0; k <= nchunks; ++k) {
+        pp.p0[k] = pairs * wacc / wsum;
+        if (k < nchunks) wacc += taper ? size_t(nchunks - k) : 1;
+    }
     pp.ws_off.assign(nchunks + 1, 0);
     for (int k = 0; k < nchunks; ++k)
         pp.ws_off[k + 1] = pp.ws_off[k] + ((wlcs::batch_workspace_bytes(
@@ -1301,7 +1311,7 @@ int wlcs_length_batch_ex(const uint8_t* xs, const uint64_t* x_off, const uint8_t
     const int kmax = batch_kmax(pairs);
     const bool bitpar = variant == WLCS_VARIANT_BITPARALLEL;
     const int nchunks =
-        bitpar ? int(std::min<size_t>(std::min<size_t>(size_t(env_int("WLCS_BATCH_CHUNKS", 4)), 64),
+        bitpar ? int(std::min<size_t>(std::min<size_t>(size_t(env_int("WLCS_BATCH_CHUNKS", 3)), 64),
                                       pairs / 8192))
                : 1;
     if (nchunks >= 2 && xs_bytes + ys_bytes >= (16u << 20)) {
