@@ -723,6 +723,28 @@ def test_batch_c2_full_against_oracle(wl, restatement):
     assert np.array_equal(got, want)
 
 
+@pytest.mark.parametrize("chunks,taper", [(2, 1), (3, 0), (5, 1), (7, 1)])
+def test_batch_pipeline_chunkings(wl, restatement, monkeypatch, chunks, taper):
+    """The host batch's copy/compute pipeline cut into 2-7 chunks, equal or
+    tapered (capi.cu batch_pipe_copies): every chunking gives the oracle's
+    lengths, long (strip-kernel) pairs included."""
+    monkeypatch.setenv("WLCS_BATCH_CHUNKS", str(chunks))
+    monkeypatch.setenv("WLCS_BATCH_TAPER", str(taper))
+    gx, gxo, gy, gyo = restatement.generate_pairs(60000, 150, 700, PROTEIN, 1234 + chunks)
+    xl = [gx[gxo[k]:gxo[k + 1]].tobytes() for k in range(60000)]
+    yl = [gy[gyo[k]:gyo[k + 1]].tobytes() for k in range(60000)]
+    # a few pairs wider than the lane shapes (finished by the strip kernel)
+    rng = np.random.default_rng(chunks)
+    al = np.frombuffer(PROTEIN, np.uint8)
+    for p in rng.choice(60000, 3, replace=False):
+        xl[p] = rng.choice(al, 12000).tobytes()
+        yl[p] = rng.choice(al, 15000).tobytes()
+    xs, xo, ys, yo = wl.pack_pairs(xl, yl)
+    got = wl.lcs_length_batch(xs, xo, ys, yo)
+    want = restatement.length_batch(xs, xo, ys, yo)
+    assert np.array_equal(got, want)
+
+
 def test_single_pair_pageable_and_pinned_inputs(wl, restatement):
     """Single-pair H2D goes through the pinned stage ring for pageable
     buffers larger than one 4 MB stage; page-locked buffers go direct."""
