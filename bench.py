@@ -534,6 +534,65 @@ def golden_length(name):
         return None
 
 
+def subsequence_pair_block(name, steps, warmup, peak_ops):
+    """C1 / C3 at full size, length + recovered subsequence through
+    lcs_subsequence (one GPU): e2e = wall time of the whole C-ABI call (H2D,
+    fill storing the bit rows, parallel traceback, D2H); fill = CUDA events
+    around the strip kernel.  The string is checked against the reference's
+    own traceback (sha256 in tests/golden/{c1.json, c3.json.gz})."""
+    import gzip
+    import hashlib
+    import paper_1306_4627_b200 as wl
+    from paper_1306_4627_b200 import workloads
+    x, y = workloads.config_pair(name)
+    cells = len(x) * len(y)
+    fn = lambda: wl.lcs_subsequence(x, y, wl.NO_BUDGET)  # noqa: E731
+    for _ in range(warmup):
+        sub = fn()
+    wl._check(wl.lib.wlcs_set_timing(1))
+    km = ctypes.c_float()
+    times, fills = [], []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        sub = fn()
+        times.append(time.perf_counter() - t0)
+        wl._check(wl.lib.wlcs_last_kernel_ms(ctypes.byref(km)))
+        fills.append(km.value)
+    wl._check(wl.lib.wlcs_set_timing(0))
+    fill_ms, wall_s = float(np.mean(fills)), float(np.mean(times))
+    try:
+        path = os.path.join(ROOT, "tests", "golden", "c1.json" if name == "c1" else "c3.json.gz")
+        opener = gzip.open if path.endswith(".gz") else open
+        with opener(path, "rt") as f:
+            want = json.load(f)["sha256"]
+    except (OSError, KeyError, ValueError):
+        want = None
+    got = hashlib.sha256(sub).hexdigest()
+    if want is not None and got != want:
+        raise AssertionError(f"EquivalenceError: {name} subsequence differs from the reference's")
+    achieved = cells * 3.0 / 32.0 / (fill_ms * 1e-3) / 1e12 if fill_ms > 0 else 0.0
+    return {"workload": {"c1": "C1: 10k x 10k DNA, length + subsequence",
+                         "c3": "C3: 100k x ~100k mutated DNA, length + subsequence"}[name],
+            "m": len(x), "n": len(y), "lcs_length": len(sub),
+            "golden_match": want is not None and got == want,
+            "n_gpus": 1, "fill_ms": round(fill_ms, 3),
+            "value": round(cells / wall_s / 1e9, 1), "unit": UNIT,
+            "e2e": {"value": round(cells / wall_s / 1e9, 1), "unit": UNIT,
+                    "ms_per_step": round(wall_s * 1e3, 3),
+                    "h2d_bytes_per_step": len(x) + len(y), "d2h_bytes_per_step": len(sub) + 8},
+            "roofline": {"bound": "int (latency: one row chain)", "achieved": round(achieved, 3),
+                         "peak": round(peak_ops / 1e12, 3), "unit": "Tops/s",
+                         "frac": round(achieved / (peak_ops / 1e12), 4),
+                         "kernel": "pair_strip_kernel (bit rows stored) + walk",
+                         # the bound that applies: every row depends on the one
+                         # above; 3 dependent ALU ops x ~4.7 cycles per row
+                         # (tools/micro/dpx_latency.cu) at the max SM clock
+                         "critical_path_ms": round(len(x) * 14.0 / 1.965e6, 3),
+                         "frac_of_critical_path": round(len(x) * 14.0 / 1.965e6 / fill_ms, 3)
+                         if fill_ms > 0 else None},
+            "steps": steps}
+
+
 def single_pair_block(name, steps, warmup, dist, peak_ops):
     """C4 / C5 at full size, length only (N = 1: one GPU; N > 1: C4's column
     split across the ranks).  Device fill time from CUDA events around the
@@ -734,6 +793,12 @@ def main():
                     line[name] = single_pair_block(name, 3, 1, dist, peak.value)
                 except Exception as exc:  # report, never lose the headline line
                     line[name] = {"error": f"{type(exc).__name__}: {exc}"}
+            if dist.world == 1:
+                for name in ("c1", "c3"):  # one-GPU configurations (configs[0], [2])
+                    try:
+                        line[name] = subsequence_pair_block(name, 5, 2, peak.value)
+                    except Exception as exc:
+                        line[name] = {"error": f"{type(exc).__name__}: {exc}"}
     elif (dist.world > 1 or args.colsplit) and args.config in ("c4", "c5"):
         line = run_colsplit(args, dist)
     else:
