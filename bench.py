@@ -579,6 +579,7 @@ def subsequence_pair_block(name, steps, warmup, peak_ops):
             "value": round(cells / wall_s / 1e9, 1), "unit": UNIT,
             "e2e": {"value": round(cells / wall_s / 1e9, 1), "unit": UNIT,
                     "ms_per_step": round(wall_s * 1e3, 3),
+                    "ms_median": round(float(np.median(times)) * 1e3, 3),
                     "h2d_bytes_per_step": len(x) + len(y), "d2h_bytes_per_step": len(sub) + 8},
             "roofline": {"bound": "int (latency: one row chain)", "achieved": round(achieved, 3),
                          "peak": round(peak_ops / 1e12, 3), "unit": "Tops/s",
@@ -603,6 +604,7 @@ def single_pair_block(name, steps, warmup, dist, peak_ops):
     x, y = workloads.config_pair(name)
     cells = len(x) * len(y)
     colsplit = dist.world > 1 and name == "c4"
+    times = []
     if colsplit:
         fill_ms, wall_s, length = colsplit_steps(wl, x, y, steps, warmup, dist)
     else:
@@ -634,6 +636,7 @@ def single_pair_block(name, steps, warmup, dist, peak_ops):
             "unit": UNIT,
             "e2e": {"value": round(cells / wall_s / 1e9, 1), "unit": UNIT,
                     "ms_per_step": round(wall_s * 1e3, 3),
+                    "ms_median": round(float(np.median(times)) * 1e3, 3) if times else None,
                     "h2d_bytes_per_step": len(x) + len(y), "d2h_bytes_per_step": 8},
             "roofline": {"bound": "int", "achieved": round(achieved, 3),
                          "peak": round(peak_ops / 1e12, 3), "unit": "Tops/s",
