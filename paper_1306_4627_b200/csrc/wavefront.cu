@@ -49,6 +49,8 @@ constexpr uint32_t kSentinel = 0x100u;    // column code of no column
 constexpr uint32_t kNoRow = 0x1ffu;       // row code past the last row
 constexpr int kWaveWarps = 4;             // warps per CTA (batch kernel)
 constexpr int kRebaseMask = 8191;
+// Build-time switches; the defaults are the measured best, the others are kept
+// so that the A/B rows of DESIGN.md section 4 can be re-run (tools/exp_build.sh)
 #ifndef WLCS_WAVE_SLEEP_NS
 #define WLCS_WAVE_SLEEP_NS 200
 #endif
