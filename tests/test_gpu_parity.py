@@ -646,8 +646,8 @@ def test_length_device_honours_stream(wl, restatement):
         d_x = torch.zeros(len(x) + 16, dtype=torch.uint8, device=dev)
         d_y = torch.zeros(len(y) + 16, dtype=torch.uint8, device=dev)
         torch.cuda._sleep(20_000_000)  # keep the side stream busy before the copies land
-        d_x[: len(x)].copy_(torch.from_numpy(np.frombuffer(x, np.uint8)))
-        d_y[: len(y)].copy_(torch.from_numpy(np.frombuffer(y, np.uint8)))
+        d_x[: len(x)].copy_(torch.from_numpy(np.frombuffer(x, np.uint8).copy()))
+        d_y[: len(y)].copy_(torch.from_numpy(np.frombuffer(y, np.uint8).copy()))
         out = ctypes.c_uint32()
         wl._check(wl.lib.wlcs_length_device(d_x.data_ptr(), len(x), d_y.data_ptr(), len(y),
                                             wl.VARIANT_BITPARALLEL, ctypes.byref(out),
