@@ -299,6 +299,25 @@ def test_wavefront_batch_edges(wl, restatement):
     check_batch_variant(wl, restatement, xs, ys, wl.VARIANT_WAVEFRONT)
 
 
+def test_wavefront_batch_bands_and_rows_per_lane(wl, restatement):
+    """The DPX batch kernel's band structure: every rows-per-lane value R = 4..16
+    (rows 1..1024 in one band), several bands per pair (rows > 1024, the
+    boundary row handed through shared memory), and the column limit (2048)
+    on both sides of it (wider pairs go to the pair kernel)."""
+    rng = np.random.default_rng(4242)
+    xs, ys = [], []
+    for rows in list(range(1, 1100, 37)) + [1024, 1025, 2048, 2049, 3000, 5000]:
+        for alphabet in (DNA, PROTEIN):
+            al = np.frombuffer(alphabet, np.uint8)
+            n = int(rng.integers(1, min(rows, 2048) + 1))
+            xs.append(rng.choice(al, rows).tobytes())
+            ys.append(rng.choice(al, n).tobytes())
+    for n in (2047, 2048, 2049):
+        xs.append(rng.choice(np.frombuffer(DNA, np.uint8), 3000).tobytes())
+        ys.append(rng.choice(np.frombuffer(DNA, np.uint8), n).tobytes())
+    check_batch_variant(wl, restatement, xs, ys, wl.VARIANT_WAVEFRONT)
+
+
 @pytest.mark.parametrize("m,n", [(1, 1), (127, 129), (129, 127), (1000, 1000), (4096, 33),
                                  (5000, 200), (20000, 7000), (150000, 70000)])
 def test_wavefront_pair(wl, restatement, m, n):
