@@ -60,6 +60,9 @@ constexpr int kRebaseMask = 8191;
 #ifndef WLCS_WAVE_MAX2
 #define WLCS_WAVE_MAX2 0
 #endif
+#ifndef WLCS_WAVE_PAIR_WARPS
+#define WLCS_WAVE_PAIR_WARPS 4
+#endif
 
 // One packed cell pair.  WLCS_WAVE_MAX2: the three-way max as two two-way
 // VIMNMX.16x2, which also issue on the FMA pipe (the ALU pipe keeps LOP3 and
@@ -289,7 +292,7 @@ __device__ __forceinline__ void st_relaxed_if(bool pred, uint32_t* p, uint32_t v
 }
 
 template <int R>
-__global__ void __launch_bounds__(32) wave_pair_kernel(WavePairDev d) {
+__global__ void __launch_bounds__(32 * WLCS_WAVE_PAIR_WARPS) wave_pair_kernel(WavePairDev d) {
     const int lane = int(lane_id());
     const int64_t n = d.n, m = d.m;
     constexpr int kBand = 64 * R;
@@ -398,15 +401,19 @@ int64_t wave_pair_bands(int64_t m, int R) { return (m + 64 * R - 1) / (64 * R); 
 
 template <int R>
 cudaError_t wave_pair_launch_r(const WavePairDev& d, int sms, cudaStream_t stream) {
+    // CTAs of WLCS_WAVE_PAIR_WARPS one-band warps: a CTA's warps sit on
+    // distinct sub-partitions, so bands spread evenly over them
+    constexpr int W = WLCS_WAVE_PAIR_WARPS;
     int occ = 0;
     cudaError_t e =
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, wave_pair_kernel<R>, 32, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, wave_pair_kernel<R>, 32 * W, 0);
     if (e != cudaSuccess) return e;
     if (occ < 1) occ = 1;
-    int64_t grid = int64_t(sms) * (occ < 16 ? occ : 16);
+    int64_t grid = int64_t(sms) * (occ * W < 16 ? occ : 16 / W);
     const int64_t bands = wave_pair_bands(d.m, R);
-    if (grid > bands) grid = bands;
-    wave_pair_kernel<R><<<int(grid), 32, 0, stream>>>(d);
+    const int64_t need = (bands + W - 1) / W;
+    if (grid > need) grid = need;
+    wave_pair_kernel<R><<<int(grid), 32 * W, 0, stream>>>(d);
     return cudaGetLastError();
 }
 
