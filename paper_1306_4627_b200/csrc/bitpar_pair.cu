@@ -733,22 +733,56 @@ __global__ void __launch_bounds__(32 * kWalkWarps) walk_emit_kernel(PairDev d, c
 }
 
 // 4a. one thread: output offsets (forward order = blocks from the top rows)
-__global__ void walk_scan_kernel(const uint32_t* counts, int64_t nb, uint32_t* offsets,
-                                 unsigned long long* total, unsigned long long* place,
-                                 unsigned long long* base) {
-    unsigned long long run = 0;
-    for (int64_t k = nb - 1; k >= 0; --k) {
+__global__ void __launch_bounds__(1024) walk_scan_kernel(const uint32_t* counts, int64_t nb,
+                                                        uint32_t* offsets,
+                                                        unsigned long long* total,
+                                                        unsigned long long* place,
+                                                        unsigned long long* base) {
+    // offsets[k] = bytes emitted by blocks above k (rows nearer the top come
+    // later in the walk but earlier in the string): a suffix-exclusive scan,
+    // one 1024-thread block (thread t owns positions r = nb-1-k in
+    // [t per, (t+1) per)), so the block counts are loaded in parallel
+    __shared__ unsigned long long wsum[32];
+    const int t = int(threadIdx.x), lane = t & 31, warp = t >> 5;
+    const int64_t per = (nb + 1023) / 1024;
+    const int64_t r0 = int64_t(t) * per, r1 = r0 + per < nb ? r0 + per : nb;
+    unsigned long long local = 0;
+    for (int64_t r = r0; r < r1; ++r) local += counts[nb - 1 - r];
+    unsigned long long incl = local;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long v = __shfl_up_sync(kFullMask, incl, o);
+        if (lane >= o) incl += v;
+    }
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        const unsigned long long ws = wsum[lane];
+        unsigned long long wi = ws;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long v = __shfl_up_sync(kFullMask, wi, o);
+            if (lane >= o) wi += v;
+        }
+        wsum[lane] = wi - ws;  // exclusive warp offsets
+    }
+    __syncthreads();
+    unsigned long long run = wsum[warp] + incl - local;
+    for (int64_t r = r0; r < r1; ++r) {
+        const int64_t k = nb - 1 - r;
         offsets[k] = uint32_t(run);
         run += counts[k];
     }
-    *total = run;
-    // banded traceback: this band's bytes end where the lower bands' begin
-    unsigned long long b = 0;
-    if (place) {
-        b = place[0] - place[1] - run;
-        place[1] += run;
+    if (t == 1023) {
+        *total = run;
+        // banded traceback: this band's bytes end where the lower bands' begin
+        unsigned long long b = 0;
+        if (place) {
+            b = place[0] - place[1] - run;
+            place[1] += run;
+        }
+        *base = b;
     }
-    *base = b;
 }
 
 // 4b. one warp per block writes its emitted bytes in row order: lane t
@@ -1057,7 +1091,7 @@ cudaError_t pair_walk(const PairDev& d, int K, const uint8_t* x, uint8_t* out,
         mark(2);
         emit<<<emit_ctas, 32 * kWalkWarps, 0, stream>>>(d, entry, flags, counts);
         mark(3);
-        walk_scan_kernel<<<1, 1, 0, stream>>>(counts, nb, offsets, out_len,
+        walk_scan_kernel<<<1, 1024, 0, stream>>>(counts, nb, offsets, out_len,
                                               d.prob[0].walk_place, base);
         walk_write_kernel<<<emit_ctas, 128, 0, stream>>>(x, M, flags, offsets, base, out);
         mark(4);
