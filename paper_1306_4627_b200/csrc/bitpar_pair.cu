@@ -639,32 +639,41 @@ __global__ void __launch_bounds__(32) walk_resolve_kernel(PairDev d, const int32
         const int32_t* ex = exits + k * kWalkCand;
         int64_t next = -1;
         // bracketing candidates (candidate columns are non-decreasing in l),
-        // l in [l0 - 1, l0 + 1]: lane t tests candidates 4t .. 4t+3 at once;
-        // any candidate that qualifies gives the true exit
-        {
-            const int64_t l0 = (j - walk_cand(g, 0, N)) / kWalkStride;
-            const int4 e4 = *reinterpret_cast<const int4*>(exl + 4 * lane);
-            const int32_t e5 = lane < 31 ? exl[4 * lane + 4] : e4.w;
-            const int32_t ev[5] = {e4.x, e4.y, e4.z, e4.w, e5};
-            int found = -1;
+        // l in [l0 - 1, l0 + 1], lowest first: the first that qualifies gives
+        // the true exit.  One lane, 32-bit column arithmetic (columns < 2^31):
+        // this step is the resolve's serial chain (one per block), so it is
+        // kept short -- no ballot, one broadcast
+        if (lane == 0) {
+            const int gi = int(g), Ni = int(N), ji = int(j);
+            auto cand = [&](int l) {
+                const int c = gi + (l - kWalkCand / 2) * kWalkStride;
+                return c < 0 ? 0 : (c > Ni ? Ni : c);
+            };
+            // fast path: no clamping around the entry -- l follows from j
+            const int c0 = gi - (kWalkCand / 2) * kWalkStride;  // unclamped candidate 0
+            const int off = ji - c0;
+            const int lf = off >> 4;  // kWalkStride = 16
+            if (off >= 0 && lf + 1 < kWalkCand && c0 + lf * kWalkStride > 0 &&
+                c0 + (lf + 1) * kWalkStride < Ni) {
+                const int32_t ea = exl[lf], eb = exl[lf + 1];
+                if ((off & (kWalkStride - 1)) == 0 || ea == eb) next = ea;
+            }
+            const int l0 = (ji - cand(0)) / kWalkStride;
 #pragma unroll
-            for (int sub = 0; sub < 4; ++sub) {
-                const int64_t l = 4 * lane + sub;
-                if (found < 0 && l >= l0 - 1 && l <= l0 + 1) {
-                    const int64_t ca = walk_cand(g, int(l), N);
-                    if (ca == j ||
-                        (l + 1 < kWalkCand && ca < j && j < walk_cand(g, int(l + 1), N) &&
-                         ev[sub] == ev[sub + 1]))
-                        found = sub;
+            for (int dl = -1; dl <= 1; ++dl) {
+                const int l = l0 + dl;
+                if (next < 0 && l >= 0 && l < kWalkCand) {
+                    const int ca = cand(l);
+                    if (ca == ji) {
+                        next = exl[l];
+                    } else if (l + 1 < kWalkCand && ca < ji && ji < cand(l + 1) &&
+                               exl[l] == exl[l + 1]) {
+                        next = exl[l];
+                    }
                 }
             }
-            const uint32_t any = __ballot_sync(kFullMask, found >= 0);
-            if (any) {
-                const int src = __ffs(any) - 1;
-                const int fs = __shfl_sync(kFullMask, found, src);
-                next = exl[4 * src + fs];
-            }
         }
+        next = __shfl_sync(kFullMask, next, 0);
         if (__all_sync(kFullMask, next < 0)) {
             // Outside the window or the bracket had not merged at the block's
             // end: walk from the true entry, but stop at the first checkpoint
@@ -1099,8 +1108,12 @@ cudaError_t pair_walk(const PairDev& d, int K, const uint8_t* x, uint8_t* out,
             cudaEventSynchronize(ev[4]);
             float t[4];
             for (int i = 0; i < 4; ++i) cudaEventElapsedTime(&t[i], ev[i], ev[i + 1]);
-            fprintf(stderr, "wlcs walk ms: spec %.3f resolve %.3f emit %.3f scan+write %.3f\n", t[0],
-                    t[1], t[2], t[3]);
+            uint32_t ms[3] = {0, 0, 0};
+            cudaMemcpy(ms, misses, sizeof(ms), cudaMemcpyDeviceToHost);
+            fprintf(stderr,
+                    "wlcs walk ms: spec %.3f resolve %.3f emit %.3f scan+write %.3f; blocks %lld, "
+                    "resolve misses %u (%u of %u kcycles)\n",
+                    t[0], t[1], t[2], t[3], (long long)nb, ms[0], ms[1], ms[2]);
         }
         return cudaGetLastError();
     };
