@@ -284,6 +284,18 @@ __device__ __forceinline__ void load_pm_sh(uint32_t a, uint32_t* P) {
     }
 }
 
+// map_a + byte r of w as ONE instruction on the FMA pipe: dp4a(w, 1 << 8r,
+// map_a) = byte_r(w) * 1 + map_a.  The row update saturates the ALU pipe;
+// PRMT (byte extract) would be an ALU op per row plus an add
+// (tools/micro/byte_extract.cu: DP4A issues on the FMA pipe at the full
+// 64 ops/clk/SM, 4.7-cycle latency, like PRMT).
+template <int R>
+__device__ __forceinline__ uint32_t byte_addr(uint32_t w, uint32_t base) {
+    uint32_t a;
+    asm("dp4a.u32.u32 %0, %1, %2, %3;" : "=r"(a) : "r"(w), "n"(1u << (8 * R)), "r"(base));
+    return a;
+}
+
 // rows8 over shared addresses: map_a = byte -> code table, pm_a = this
 // lane's word 0 of code 0.
 template <bool CHAIN, int K>
@@ -291,10 +303,14 @@ __device__ __forceinline__ void rows8_sh(uint32_t* V, uint32_t map_a, uint32_t p
                                          uint32_t hi, uint32_t& cin, uint32_t& cout) {
     constexpr uint32_t cs = PmLayout<K>::code_stride;
     uint32_t off[8];
-#pragma unroll
-    for (int r = 0; r < 8; ++r)
-        off[r] = lds_u8(map_a + __byte_perm(r < 4 ? lo : hi, 0u, 0x4440u | uint32_t(r & 3))) * cs +
-                 pm_a;
+    off[0] = lds_u8(byte_addr<0>(lo, map_a)) * cs + pm_a;
+    off[1] = lds_u8(byte_addr<1>(lo, map_a)) * cs + pm_a;
+    off[2] = lds_u8(byte_addr<2>(lo, map_a)) * cs + pm_a;
+    off[3] = lds_u8(byte_addr<3>(lo, map_a)) * cs + pm_a;
+    off[4] = lds_u8(byte_addr<0>(hi, map_a)) * cs + pm_a;
+    off[5] = lds_u8(byte_addr<1>(hi, map_a)) * cs + pm_a;
+    off[6] = lds_u8(byte_addr<2>(hi, map_a)) * cs + pm_a;
+    off[7] = lds_u8(byte_addr<3>(hi, map_a)) * cs + pm_a;
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
         uint32_t P[K];

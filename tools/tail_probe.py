@@ -7,7 +7,7 @@ if len(sys.argv) > 1 and sys.argv[1] == "run":
     import torch
     import paper_1306_4627_b200 as wl
     import bench
-    xs, xo, ys, yo = bench.gen_pairs(wl, 65536, 200, 1000, bench.PROTEIN, 1, pinned=False)
+    xs, xo, ys, yo = (np.array(a) for a in bench.gen_pairs_pinned(wl, 65536, 200, 1000, bench.PROTEIN, 1))
     dev = torch.device("cuda")
     d_xs = torch.from_numpy(xs[: int(xo[-1]) + 16]).to(dev)
     d_ys = torch.from_numpy(ys[: int(yo[-1]) + 16]).to(dev)

@@ -8,7 +8,8 @@ import torch
 import paper_1306_4627_b200 as wl
 import bench
 
-xs, xo, ys, yo = bench.gen_pairs(wl, 65536, 200, 1000, bench.PROTEIN, 20130619, pinned=False)
+xs, xo, ys, yo = bench.gen_pairs_pinned(wl, 65536, 200, 1000, bench.PROTEIN, 20130619)
+xs, xo, ys, yo = (np.array(a) for a in (xs, xo, ys, yo))
 dev = torch.device("cuda")
 d_xs = torch.from_numpy(xs[: int(xo[-1]) + 16]).to(dev)
 d_ys = torch.from_numpy(ys[: int(yo[-1]) + 16]).to(dev)
