@@ -341,48 +341,63 @@ __device__ __forceinline__ int lane_zero_count(const uint32_t* V, int64_t word0,
 // Match-mask build helpers (batch kernels): 32 column bytes -> 8 bit-planes.
 // Each lane owns 32-column words of its pair's column string; per word it
 // (1) realigns the 32 column bytes out of 16-byte aligned chunks (funnel
-// shifts), (2) turns them into 8 bit-planes with four 8x8 bit transposes
-// (plane b, bit j = bit b of column j's byte).  A code's match mask is then
-// the AND over the planes of "plane == bit of the code's byte value".
-__device__ __forceinline__ uint64_t transpose8x8(uint64_t x) {
-    uint64_t t = (x ^ (x >> 7)) & 0x00AA00AA00AA00AAull;
-    x = x ^ t ^ (t << 7);
-    t = (x ^ (x >> 14)) & 0x0000CCCC0000CCCCull;
-    x = x ^ t ^ (t << 14);
-    t = (x ^ (x >> 28)) & 0x00000000F0F0F0F0ull;
-    return x ^ t ^ (t << 28);
+// shifts), (2) turns them into 8 bit-planes (plane b, bit j = bit b of
+// column j's byte).  A code's match mask is then the AND over the planes of
+// "plane == bit of the code's byte value".
+//
+// bit_planes8: 16 PRMT regroup the bytes by column stride 8 (word i holds
+// columns i, i+8, i+16, i+24 as its bytes 0..3), then three delta swaps
+// exchange the word-index bits (i2 i1 i0) with the in-byte bit index
+// (b2 b1 b0): afterwards word b holds bit b of column 8k + i at position
+// 8k + i.  76 ALU ops per word (the 8x8 transposes were ~110).
+__device__ __forceinline__ void delta_swap(uint32_t& x, uint32_t& y, int d, uint32_t keep) {
+    const uint32_t t = ((x >> d) ^ y) & keep;  // keep = positions whose bit s is 0
+    y ^= t;
+    x ^= t << d;
 }
 
-// 32 column bytes (8 words, byte j of the word = column j) -> 8 bit-planes.
 __device__ __forceinline__ void bit_planes8(const uint32_t* w, uint32_t* P) {
-    uint32_t lo[4], hi[4];
+    uint32_t g[8];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        const uint64_t y = transpose8x8(uint64_t(w[2 * q]) | (uint64_t(w[2 * q + 1]) << 32));
-        lo[q] = uint32_t(y);          // planes 0..3, 8 columns each
-        hi[q] = uint32_t(y >> 32);    // planes 4..7
+    for (int h = 0; h < 2; ++h) {
+#pragma unroll
+        for (int m = 0; m < 4; m += 2) {
+            // bytes m and m+1 of w[h], w[h+2] / w[h+4], w[h+6]
+            const uint32_t sel = uint32_t(m) | uint32_t(4 + m) << 4 | uint32_t(m + 1) << 8 |
+                                 uint32_t(5 + m) << 12;
+            const uint32_t t1 = __byte_perm(w[h], w[h + 2], sel);
+            const uint32_t t2 = __byte_perm(w[h + 4], w[h + 6], sel);
+            g[4 * h + m] = __byte_perm(t1, t2, 0x5410);      // columns c, c+8, c+16, c+24
+            g[4 * h + m + 1] = __byte_perm(t1, t2, 0x7632);  // c = 4h + m (+1)
+        }
+    }
+    // word index i = 4h + m; stage s pairs words i and i + 2^s
+#pragma unroll
+    for (int i = 0; i < 8; i += 2) delta_swap(g[i], g[i + 1], 1, 0x55555555u);
+#pragma unroll
+    for (int i = 0; i < 8; i += 4) {
+        delta_swap(g[i], g[i + 2], 2, 0x33333333u);
+        delta_swap(g[i + 1], g[i + 3], 2, 0x33333333u);
     }
 #pragma unroll
-    for (int b = 0; b < 4; ++b) {
-        const uint32_t sel = 0x0040u | uint32_t(b) | (uint32_t(b) << 4);  // bytes b of x, y
-        P[b] = __byte_perm(__byte_perm(lo[0], lo[1], sel), __byte_perm(lo[2], lo[3], sel), 0x5410);
-        P[b + 4] =
-            __byte_perm(__byte_perm(hi[0], hi[1], sel), __byte_perm(hi[2], hi[3], sel), 0x5410);
-    }
+    for (int i = 0; i < 4; ++i) delta_swap(g[i], g[i + 4], 4, 0x0f0f0f0fu);
+#pragma unroll
+    for (int b = 0; b < 8; ++b) P[b] = g[b];
 }
 
 // The 32 column bytes of the lane's word k, realigned out of the 16-byte
-// aligned chunks 2k, 2k+1, 2k+2 (q = a_c / 4, fs = 8 * (a_c % 4)).
+// aligned chunks 2k, 2k+1, 2k+2 (q = a_c / 4, fs = 8 * (a_c % 4)): word i is
+// the funnel shift of W[i + q] and W[i + q + 1]; W[i + q] is picked with two
+// selects (odd q, then q >= 2).
 __device__ __forceinline__ void word_bytes(const uint4& c0, const uint4& c1, const uint4& c2, int q,
                                            uint32_t fs, uint32_t* w) {
     const uint32_t W[12] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w, c2.x, c2.y, c2.z, c2.w};
+    uint32_t a[11];
+#pragma unroll
+    for (int i = 0; i < 11; ++i) a[i] = (q & 1) ? W[i + 1] : W[i];
     uint32_t lo[9];
 #pragma unroll
-    for (int i = 0; i < 9; ++i) {
-        const uint32_t a = (q & 1) ? W[i + 1] : W[i];
-        const uint32_t b2 = (q & 1) ? W[i + 3] : W[i + 2];
-        lo[i] = (q & 2) ? b2 : a;
-    }
+    for (int i = 0; i < 9; ++i) lo[i] = (q & 2) ? a[i + 2] : a[i];
 #pragma unroll
     for (int i = 0; i < 8; ++i) w[i] = __funnelshift_r(lo[i], lo[i + 1], fs);
 }

@@ -51,3 +51,5 @@ print("busy warps per 10 us bin:", " ".join(f"{x:.0f}" for x in busy))
 o = np.argsort(-b)[:8]
 for i in o:
     print(f"  late task S={cls[i]//16} K={cls[i]%16} start {a[i]/1e3:.1f} end {b[i]/1e3:.1f} rows {rows[i]}")
+np.savez(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "gpurun_out", "trace.npz"),
+         a=a, b=b, sm=sm, bld=bld, cls=cls, rows=rows)
