@@ -357,6 +357,62 @@ struct MapState {
     uint32_t zrep;   // a byte absent from the map, replicated x4
 };
 
+// Dense codes 1..sigma-1 in byte order (0 = no match) for the byte set
+// `present` (lane l holds bytes 8l .. 8l+7 as bits 0..7): writes the
+// byte -> code map and the low-nibble presence per high nibble (inv), and
+// returns sigma (codes incl. the zero row), the ballot of present high
+// nibbles (bit 2h) and a byte absent from the set replicated x4.  False when
+// more than 255 codes would be needed.
+__device__ __forceinline__ bool assign_codes(uint32_t present, uint32_t map, uint32_t inv,
+                                             uint32_t* sigma, uint32_t* hm, uint32_t* zrep) {
+    const uint32_t lane = lane_id();
+    const uint32_t cnt = __popc(present);
+    uint32_t incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(kFullMask, incl, o);
+        if (int(lane) >= o) incl += v;
+    }
+    *sigma = __shfl_sync(kFullMask, incl, 31) + 1;  // + the zero row
+    if (*sigma > 256u) return false;
+    uint32_t code = incl - cnt + 1;
+    uint32_t ox = 0, oy = 0;
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+        if ((present >> b) & 1u) {
+            if (b < 4) ox |= code << (8 * b);
+            else oy |= code << (8 * (b - 4));
+            ++code;
+        }
+    }
+    // low-nibble presence per high nibble h (lanes 2h, 2h+1 hold bytes 16h..16h+15)
+    const uint32_t upper = __shfl_down_sync(kFullMask, present, 1);
+    const uint32_t nib16 = present | (upper << 8);
+    *hm = __ballot_sync(kFullMask, (lane & 1u) == 0u && nib16 != 0u);
+    const uint32_t absent = ~present & 0xffu;  // exists: at most 255 bytes present
+    const uint32_t has = __ballot_sync(kFullMask, absent != 0u);
+    const uint32_t zb = __shfl_sync(kFullMask, uint32_t(8 * lane) + __ffs(absent) - 1, __ffs(has) - 1);
+    *zrep = zb * 0x01010101u;
+    __syncwarp();
+    sts_v2(map + 8u * lane, ox, oy);
+    if ((lane & 1u) == 0u) sts_u16(inv + lane, nib16);
+    return true;
+}
+
+// Presence flags (one 32-bit word per byte value at `flags`) of the valid
+// bytes (bit r of vm) of a 16-byte chunk.
+__device__ __forceinline__ void mark_chunk(const uint4& c, uint32_t vm, uint32_t flags) {
+    const uint32_t w[4] = {c.x, c.y, c.z, c.w};
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+        if ((vm >> r) & 1u) {
+            uint32_t a;
+            asm("dp4a.u32.u32 %0, %1, %2, %3;" : "=r"(a) : "r"(w[r >> 2]), "r"(4u << (8 * (r & 3))), "r"(flags));
+            sts_u32(a, 1u);
+        }
+    }
+}
+
 // Builds the task's match masks (and, when needed, its byte -> code map) in
 // shared memory.  K is a runtime value and every loop over words / codes is
 // rolled: the build is one small piece of code shared by all lane shapes (it
@@ -403,10 +459,36 @@ __device__ __forceinline__ uint32_t build_task(const BatchDev& d, const LanePair
     };
     uint32_t sigma = st.sigma, hm = st.hm;
     *zrep = st.zrep;
-    // attempt 0: the previous task's map; attempt 1: a fresh map
-    int attempt = (hm != 0u && sigma * cs <= uint32_t(d.pm_bytes)) ? 0 : 1;
-    for (;; ++attempt) {
+    // attempt 0: the previous task's map; attempt 2 (a warp's first task): a
+    // map sampled from the first 32 column bytes of every lane; attempt 1 (a
+    // column byte missing from the map): a fresh map from all columns
+    int attempt = (hm != 0u && sigma * cs <= uint32_t(d.pm_bytes)) ? 0 : (hm == 0u ? 2 : 1);
+    for (;;) {
         bool use_stage = false;
+        if (attempt == 2) {
+            const uint32_t flags = pm;
+            __syncwarp();
+#pragma unroll
+            for (int i = 0; i < 2; ++i) sts_v4(flags + 16u * (lane * 2 + i), make_uint4(0u, 0u, 0u, 0u));
+            const uint4 s0 = chunk(0), s1 = chunk(1);
+            const uint32_t v0 = valid_mask16(-a_c, clen), v1 = valid_mask16(16 - a_c, clen);
+            __syncwarp();
+            mark_chunk(s0, v0, flags);
+            mark_chunk(s1, v1, flags);
+            __syncwarp();
+            const uint4 f0 = lds_v4(flags + 32u * lane);
+            const uint4 f1 = lds_v4<16>(flags + 32u * lane);
+            const uint32_t present = (f0.x ? 1u : 0u) | (f0.y ? 2u : 0u) | (f0.z ? 4u : 0u) |
+                                     (f0.w ? 8u : 0u) | (f1.x ? 16u : 0u) | (f1.y ? 32u : 0u) |
+                                     (f1.z ? 64u : 0u) | (f1.w ? 128u : 0u);
+            __syncwarp();
+            if (!assign_codes(present, map, inv, &sigma, &hm, zrep) ||
+                sigma * cs > uint32_t(d.pm_bytes)) {
+                attempt = 1;
+                continue;
+            }
+            __syncwarp();
+        }
         if (attempt == 1) {
             // presence flags: one 32-bit word per byte value in the (not yet
             // used) PM region -- lanes marking the same byte hit the same word
@@ -470,38 +552,10 @@ __device__ __forceinline__ uint32_t build_task(const BatchDev& d, const LanePair
                 const uint32_t present = (f0.x ? 1u : 0u) | (f0.y ? 2u : 0u) | (f0.z ? 4u : 0u) |
                                          (f0.w ? 8u : 0u) | (f1.x ? 16u : 0u) | (f1.y ? 32u : 0u) |
                                          (f1.z ? 64u : 0u) | (f1.w ? 128u : 0u);  // byte 8*lane + b
-                const uint32_t cnt = __popc(present);
-                uint32_t incl = cnt;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const uint32_t v = __shfl_up_sync(kFullMask, incl, o);
-                    if (int(lane) >= o) incl += v;
-                }
-                sigma = __shfl_sync(kFullMask, incl, 31) + 1;  // + the zero row
                 st.hm = 0u;  // the map is about to change
-                if (sigma > 256u || sigma * cs > uint32_t(d.pm_bytes)) return 0u;
-                uint32_t code = incl - cnt + 1;
-                uint32_t ox = 0, oy = 0;
-#pragma unroll
-                for (int b = 0; b < 8; ++b) {
-                    if ((present >> b) & 1u) {
-                        if (b < 4) ox |= code << (8 * b);
-                        else oy |= code << (8 * (b - 4));
-                        ++code;
-                    }
-                }
-                // low-nibble presence per high nibble h (lanes 2h, 2h+1 hold bytes 16h..16h+15)
-                const uint32_t upper = __shfl_down_sync(kFullMask, present, 1);
-                const uint32_t nib16 = present | (upper << 8);
-                hm = __ballot_sync(kFullMask, (lane & 1u) == 0u && nib16 != 0u);
-                const uint32_t absent = ~present & 0xffu;  // exists: at most 255 bytes present
-                const uint32_t has = __ballot_sync(kFullMask, absent != 0u);
-                const uint32_t zb =
-                    __shfl_sync(kFullMask, uint32_t(8 * lane) + __ffs(absent) - 1, __ffs(has) - 1);
-                *zrep = zb * 0x01010101u;
-                __syncwarp();
-                sts_v2(map + 8u * lane, ox, oy);
-                if ((lane & 1u) == 0u) sts_u16(inv + lane, nib16);
+                if (!assign_codes(present, map, inv, &sigma, &hm, zrep) ||
+                    sigma * cs > uint32_t(d.pm_bytes))
+                    return 0u;
             }
             __syncwarp();
             use_stage = sigma * cs <= uint32_t(d.pm_bytes) - uint32_t(nchk) * 512u;
@@ -578,6 +632,7 @@ __device__ __forceinline__ uint32_t build_task(const BatchDev& d, const LanePair
             }
         }
         if (attempt == 1 || __all_sync(kFullMask, covered)) break;
+        attempt = 1;
     }
     __syncwarp();
     st.hm = hm;
