@@ -58,6 +58,8 @@ def test_reference_acceptance_criteria(tmp_path):
     lines = {int(m.group(1)): (m.group(2), m.group(0))
              for m in re.finditer(r"^criterion (\d): \S.*? (PASS|FAIL|SKIP) \(.*$", r.stdout, re.M)}
     assert sorted(lines) == [1, 2, 3, 4, 5, 6, 7], r.stdout + r.stderr
+    csv = tmp_path / "acceptance_table1.csv"
+    table = csv.read_text() if csv.exists() else "(no CSV)"
     for k in (1, 2, 3, 4, 5, 7):
-        assert lines[k][0] == "PASS", lines[k][1]
+        assert lines[k][0] == "PASS", lines[k][1] + "\n" + table
     print(lines[6][1])

@@ -269,11 +269,79 @@ __global__ void __launch_bounds__(32) sweep_bench4(const uint8_t* rows, int step
     out[blockIdx.x * 32 + lane] = acc;
 }
 
+// K = 10 with packed slots: words 0-3 [lane][4] at 0, words 4-7 [lane][4] at
+// 512, words 8-9 [lane][2] at 1024 (code stride 1280 as [lane][10]) -> three
+// loads per row (LDS.128, LDS.128, LDS.64) instead of five LDS.64.
+template <bool CHAIN, int S>
+__global__ void __launch_bounds__(32) sweep_bench5(const uint8_t* rows, int steps, uint32_t* out) {
+    constexpr int K = 10;
+    extern __shared__ __align__(16) uint8_t smem[];
+    const uint32_t lane = threadIdx.x & 31;
+    uint32_t sbase;
+    asm volatile("mov.b32 %0, %1;" : "=r"(sbase) : "r"(smem_u32(smem)));
+    constexpr uint32_t cs = 1280;
+    for (int b = lane; b < 256; b += 32) smem[b] = (b >= 65 && b < 65 + kSigma - 1) ? uint8_t(b - 64) : 0;
+    uint32_t x = 0x9e3779b9u * (blockIdx.x * 32 + lane + 1);
+    for (uint32_t i = lane; i < kSigma * cs / 4; i += 32) {
+        x ^= x << 13; x ^= x >> 17; x ^= x << 5;
+        reinterpret_cast<uint32_t*>(smem + kMapBytes)[i] = i < cs / 4 ? 0u : x;
+    }
+    __syncwarp();
+    const uint32_t map_a = sbase;
+    const uint32_t pm_a = sbase + kMapBytes + lane * 16u;
+    const uint32_t pm_b = sbase + kMapBytes + 1024u + lane * 8u;
+    uint32_t V[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) V[k] = 0xffffffffu;
+    const int s = int(lane) & (S - 1);
+    const uint4* rp = reinterpret_cast<const uint4*>(rows) + size_t(blockIdx.x * 32 + lane) * steps;
+    uint4 cur = ldg_l2pf(rp);
+    uint32_t cout = 0;
+    for (int t = 0; t < steps - 1; ++t) {
+        const uint4 nxt = ldg_l2pf(rp + t + 1);
+        uint32_t cin = 0;
+        if constexpr (CHAIN) {
+            cin = __shfl_up_sync(kFullMask, cout, 1, S);
+            if (s == 0) cin = 0;
+            cin <<= 16;
+            cout = 0;
+        }
+        uint32_t wlo = cur.x, whi = cur.y;
+#pragma unroll 1
+        for (int h = 0; h < 2; ++h) {
+            uint32_t code[8];
+            code[0] = lds_u8(byte_addr<0>(wlo, map_a)) * cs; code[1] = lds_u8(byte_addr<1>(wlo, map_a)) * cs;
+            code[2] = lds_u8(byte_addr<2>(wlo, map_a)) * cs; code[3] = lds_u8(byte_addr<3>(wlo, map_a)) * cs;
+            code[4] = lds_u8(byte_addr<0>(whi, map_a)) * cs; code[5] = lds_u8(byte_addr<1>(whi, map_a)) * cs;
+            code[6] = lds_u8(byte_addr<2>(whi, map_a)) * cs; code[7] = lds_u8(byte_addr<3>(whi, map_a)) * cs;
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+                uint32_t P[K];
+                const uint4 p0 = lds_v4(code[r] + pm_a);
+                const uint4 p1 = lds_v4<512>(code[r] + pm_a);
+                const uint2 p2 = lds_v2(code[r] + pm_b);
+                P[0] = p0.x; P[1] = p0.y; P[2] = p0.z; P[3] = p0.w;
+                P[4] = p1.x; P[5] = p1.y; P[6] = p1.z; P[7] = p1.w;
+                P[8] = p2.x; P[9] = p2.y;
+                if constexpr (CHAIN) RowStep<K>::chain(V, P, cin, cout);
+                else RowStep<K>::plain(V, P);
+            }
+            wlo = cur.z;
+            whi = cur.w;
+        }
+        cur = nxt;
+    }
+    uint32_t acc = cout;
+#pragma unroll
+    for (int k = 0; k < K; ++k) acc ^= V[k];
+    out[blockIdx.x * 32 + lane] = acc;
+}
+
 template <bool CHAIN, int K, int S, int AHEAD, int PIPE = 0>
 void run(const uint8_t* rows, int steps, uint32_t* out, int sms, int warps_per_sm) {
     constexpr uint32_t cs = PmLayout<K>::code_stride;
     const int smem = kMapBytes + kSigma * cs;
-    auto kern = PIPE == 3 ? sweep_bench4<CHAIN, K, S, AHEAD> : PIPE == 2 ? sweep_bench3<CHAIN, K, S, AHEAD> : PIPE ? sweep_bench2<CHAIN, K, S, AHEAD> : sweep_bench<CHAIN, K, S, AHEAD>;
+    auto kern = PIPE == 4 ? sweep_bench5<CHAIN, S> : PIPE == 3 ? sweep_bench4<CHAIN, K, S, AHEAD> : PIPE == 2 ? sweep_bench3<CHAIN, K, S, AHEAD> : PIPE ? sweep_bench2<CHAIN, K, S, AHEAD> : sweep_bench<CHAIN, K, S, AHEAD>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 48 * 1024);
     cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
     int occ = 0;
@@ -295,7 +363,7 @@ void run(const uint8_t* rows, int steps, uint32_t* out, int sms, int warps_per_s
     const double alu = double(grid) * (steps - AHEAD) * 16.0 * (3 * K + (CHAIN ? 1 : 0));
     const double cyc = ms * 1e-3 * clk * 1e3;
     printf("%s K=%2d chain=%d S=%d ahead=%d warps/SM=%2d (occ %2d, smem %5d): %.3f ms, row-update ALU %.2f /clk/SM = %.1f%% of peak\n",
-           PIPE == 3 ? "regs " : PIPE == 2 ? "nomap" : PIPE ? "pipe" : "base", K, int(CHAIN), S, AHEAD, per_sm, occ, smem, ms, alu / cyc / sms, 100.0 * alu / cyc / sms / 2.0);
+           PIPE == 4 ? "slot3" : PIPE == 3 ? "regs " : PIPE == 2 ? "nomap" : PIPE ? "pipe" : "base", K, int(CHAIN), S, AHEAD, per_sm, occ, smem, ms, alu / cyc / sms, 100.0 * alu / cyc / sms / 2.0);
 }
 
 int main() {
@@ -311,8 +379,11 @@ int main() {
     cudaMalloc(&d, h.size());
     cudaMalloc(&out, max_grid * 32 * 4);
     cudaMemcpy(d, h.data(), h.size(), cudaMemcpyHostToDevice);
-    for (int pipe = 0; pipe < 4; ++pipe) {
-        if (pipe == 3) {
+    for (int pipe = 0; pipe < 5; ++pipe) {
+        if (pipe == 4) {
+            run<false, 10, 1, 1, 4>(d, steps, out, sms, 8);
+            run<true, 10, 2, 1, 4>(d, steps, out, sms, 8);
+        } else if (pipe == 3) {
             run<false, 10, 1, 1, 3>(d, steps, out, sms, 8);
             run<false, 10, 1, 1, 3>(d, steps, out, sms, 16);
             run<true, 8, 2, 1, 3>(d, steps, out, sms, 8);
