@@ -587,9 +587,12 @@ __device__ __forceinline__ uint32_t build_task(const BatchDev& d, const LanePair
                 const int nv1 = has1 ? min(max(clen - 32 * (k + 1), 0), 32) : 0;
                 const uint32_t vm0 = nv0 >= 32 ? 0xffffffffu : ((1u << nv0) - 1u);
                 const uint32_t vm1 = nv1 >= 32 ? 0xffffffffu : ((1u << nv1) - 1u);
-                uint32_t ca0 = pm + woff_of(k), ca1 = pm + woff_of(k + 1);
-                sts_u32(ca0, 0u);  // code 0: the zero row
-                if (has1) sts_u32(ca1, 0u);
+                // words k, k+1 (k even) are adjacent and 8-byte aligned in every
+                // layout: one STS.64 per code (half the stores, at most 2-way
+                // bank conflicts where the 16-byte lane stride gave 4-way)
+                uint32_t ca0 = pm + woff_of(k);
+                if (has1) sts_v2(ca0, 0u, 0u);  // code 0: the zero row
+                else sts_u32(ca0, 0u);
                 const uint32_t a0[4] = {~(P0[0] | P0[1]), P0[0] & ~P0[1], ~P0[0] & P0[1], P0[0] & P0[1]};
                 const uint32_t b0[4] = {~(P0[2] | P0[3]), P0[2] & ~P0[3], ~P0[2] & P0[3], P0[2] & P0[3]};
                 const uint32_t a1[4] = {~(P1[0] | P1[1]), P1[0] & ~P1[1], ~P1[0] & P1[1], P1[0] & P1[1]};
@@ -612,12 +615,11 @@ __device__ __forceinline__ uint32_t build_task(const BatchDev& d, const LanePair
                             for (int ii = 0; ii < 4; ++ii) {
                                 if ((nm >> (4 * jj + ii)) & 1u) {
                                     ca0 += cs;
-                                    ca1 += cs;
                                     const uint32_t mk0 = hb0 & a0[ii], mk1 = hb1 & a1[ii];
                                     cov0 |= mk0;
                                     cov1 |= mk1;
-                                    sts_u32(ca0, mk0);
-                                    if (has1) sts_u32(ca1, mk1);
+                                    if (has1) sts_v2(ca0, mk0, mk1);
+                                    else sts_u32(ca0, mk0);
                                 }
                             }
                         }
