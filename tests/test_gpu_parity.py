@@ -78,6 +78,25 @@ def test_batch_edges(wl, restatement):
     check_batch(wl, restatement, xs, ys)
 
 
+def test_batch_sampled_map_misses(wl, restatement):
+    """A warp's first task builds with a byte -> code map sampled from the
+    first 32 column bytes of each lane.  Here every column string starts with
+    a run of one letter and holds its other letters (which the rows share)
+    only later, so the sampled map always misses bytes: the build must fall
+    back to the full presence pass and still return the oracle's lengths."""
+    rng = np.random.default_rng(4242)
+    letters = np.frombuffer(b"ACDEFGHIKLMNPQRSTVWYZ", np.uint8)
+    xs, ys = [], []
+    for i in range(3000):
+        head = int(rng.integers(33, 120))
+        tail = int(rng.integers(1, 400))
+        col = b"A" * head + letters[rng.integers(0, len(letters), tail)].tobytes()
+        row = letters[rng.integers(0, len(letters), int(rng.integers(len(col), 1100)))].tobytes()
+        xs.append(row)
+        ys.append(col)
+    check_batch(wl, restatement, xs, ys)
+
+
 def test_batch_large_alphabet_many(wl, restatement):
     """Thousands of 256-symbol pairs: their alphabets overflow the first
     pass's mask budget and take the one-word-per-lane second pass (columns
