@@ -1239,14 +1239,21 @@ int wlcs_subsequence_ex(const uint8_t* x, size_t m, const uint8_t* y, size_t n,
     // stored-row bytes of the full path (the strip plan's geometry, K = the
     // cost model's choice for a store fill)
     const int64_t W = (int64_t(n) + 31) / 32;
-    size_t limit = row_cap;
-    if (limit == 0) {
-        size_t free_b = 0, total_b = 0;
-        WLCS_CUDA(cudaMemGetInfo(&free_b, &total_b));
-        limit = std::min<size_t>(free_b / 2, size_t(8) << 30);
-    }
     // full store needs about M * 32 * ceil(W / 32 / K) * K * 4 bytes >= M * N / 8
     const double full_est = double(m + 528) * double((W + 31) / 32 * 32) * 4.0;
+    size_t limit = row_cap;
+    if (limit == 0) {
+        // automatic cap: half the free memory, at most 8 GiB.  cudaMemGetInfo
+        // costs ~70 us per call (more than a 10k x 10k fill), so it is only
+        // asked when the full store could come near the cap.
+        if (full_est <= double(size_t(1) << 30)) {
+            limit = size_t(8) << 30;
+        } else {
+            size_t free_b = 0, total_b = 0;
+            WLCS_CUDA(cudaMemGetInfo(&free_b, &total_b));
+            limit = std::min<size_t>(free_b / 2, size_t(8) << 30);
+        }
+    }
     unsigned long long len = 0;
     rc = full_est <= double(limit) ? subsequence_full(*c, dx, m, dy, n, &len)
                                    : subsequence_banded(*c, dx, m, dy, n, limit, &len);
