@@ -405,11 +405,67 @@ __global__ void __launch_bounds__(32) sweep_bench6(const uint8_t* rows, int step
     out[blockIdx.x * 32 + lane] = acc;
 }
 
+// 16-row body per step (one head latency per 16 rows instead of per 8).
+template <bool CHAIN, int K, int S, int AHEAD>
+__global__ void __launch_bounds__(32) sweep_bench7(const uint8_t* rows, int steps, uint32_t* out) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    const uint32_t lane = threadIdx.x & 31;
+    uint32_t sbase;
+    asm volatile("mov.b32 %0, %1;" : "=r"(sbase) : "r"(smem_u32(smem)));
+    constexpr uint32_t cs = PmLayout<K>::code_stride;
+    for (int b = lane; b < 256; b += 32) smem[b] = (b >= 65 && b < 65 + kSigma - 1) ? uint8_t(b - 64) : 0;
+    uint32_t x = 0x9e3779b9u * (blockIdx.x * 32 + lane + 1);
+    for (uint32_t i = lane; i < kSigma * cs / 4; i += 32) {
+        x ^= x << 13; x ^= x >> 17; x ^= x << 5;
+        reinterpret_cast<uint32_t*>(smem + kMapBytes)[i] = i < cs / 4 ? 0u : x;
+    }
+    __syncwarp();
+    const uint32_t map_a = sbase;
+    const uint32_t pm_a = sbase + kMapBytes + PmLayout<K>::word_offset(lane, 0);
+    uint32_t V[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) V[k] = 0xffffffffu;
+    const int s = int(lane) & (S - 1);
+    const uint4* rp = reinterpret_cast<const uint4*>(rows) + size_t(blockIdx.x * 32 + lane) * steps;
+    uint4 cur = ldg_l2pf(rp);
+    uint32_t cout = 0;
+    for (int t = 0; t < steps - 1; ++t) {
+        const uint4 nxt = ldg_l2pf(rp + t + 1);
+        uint32_t cin = 0;
+        if constexpr (CHAIN) {
+            cin = __shfl_up_sync(kFullMask, cout, 1, S);
+            if (s == 0) cin = 0;
+            cin <<= 16;
+            cout = 0;
+        }
+        const uint32_t w[4] = {cur.x, cur.y, cur.z, cur.w};
+        uint32_t off[16];
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+            uint32_t a;
+            asm("dp4a.u32.u32 %0, %1, %2, %3;" : "=r"(a) : "r"(w[r >> 2]), "r"(1u << (8 * (r & 3))), "r"(map_a));
+            off[r] = lds_u8(a) * cs + pm_a;
+        }
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+            uint32_t P[K];
+            load_pm_sh<K>(off[r], P);
+            if constexpr (CHAIN) RowStep<K>::chain(V, P, cin, cout);
+            else RowStep<K>::plain(V, P);
+        }
+        cur = nxt;
+    }
+    uint32_t acc = cout;
+#pragma unroll
+    for (int k = 0; k < K; ++k) acc ^= V[k];
+    out[blockIdx.x * 32 + lane] = acc;
+}
+
 template <bool CHAIN, int K, int S, int AHEAD, int PIPE = 0>
 void run(const uint8_t* rows, int steps, uint32_t* out, int sms, int warps_per_sm) {
     constexpr uint32_t cs = PmLayout<K>::code_stride;
     const int smem = kMapBytes + kSigma * cs;
-    auto kern = PIPE == 5 ? sweep_bench6<CHAIN, K, S, AHEAD> : PIPE == 4 ? sweep_bench5<CHAIN, S> : PIPE == 3 ? sweep_bench4<CHAIN, K, S, AHEAD> : PIPE == 2 ? sweep_bench3<CHAIN, K, S, AHEAD> : PIPE ? sweep_bench2<CHAIN, K, S, AHEAD> : sweep_bench<CHAIN, K, S, AHEAD>;
+    auto kern = PIPE == 6 ? sweep_bench7<CHAIN, K, S, AHEAD> : PIPE == 5 ? sweep_bench6<CHAIN, K, S, AHEAD> : PIPE == 4 ? sweep_bench5<CHAIN, S> : PIPE == 3 ? sweep_bench4<CHAIN, K, S, AHEAD> : PIPE == 2 ? sweep_bench3<CHAIN, K, S, AHEAD> : PIPE ? sweep_bench2<CHAIN, K, S, AHEAD> : sweep_bench<CHAIN, K, S, AHEAD>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 48 * 1024);
     cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
     int occ = 0;
@@ -431,7 +487,7 @@ void run(const uint8_t* rows, int steps, uint32_t* out, int sms, int warps_per_s
     const double alu = double(grid) * (steps - AHEAD) * 16.0 * (3 * K + (CHAIN ? 1 : 0));
     const double cyc = ms * 1e-3 * clk * 1e3;
     printf("%s K=%2d chain=%d S=%d ahead=%d warps/SM=%2d (occ %2d, smem %5d): %.3f ms, row-update ALU %.2f /clk/SM = %.1f%% of peak\n",
-           PIPE == 5 ? "range" : PIPE == 4 ? "slot3" : PIPE == 3 ? "regs " : PIPE == 2 ? "nomap" : PIPE ? "pipe" : "base", K, int(CHAIN), S, AHEAD, per_sm, occ, smem, ms, alu / cyc / sms, 100.0 * alu / cyc / sms / 2.0);
+           PIPE == 6 ? "full16" : PIPE == 5 ? "range" : PIPE == 4 ? "slot3" : PIPE == 3 ? "regs " : PIPE == 2 ? "nomap" : PIPE ? "pipe" : "base", K, int(CHAIN), S, AHEAD, per_sm, occ, smem, ms, alu / cyc / sms, 100.0 * alu / cyc / sms / 2.0);
 }
 
 int main() {
@@ -447,8 +503,15 @@ int main() {
     cudaMalloc(&d, h.size());
     cudaMalloc(&out, max_grid * 32 * 4);
     cudaMemcpy(d, h.data(), h.size(), cudaMemcpyHostToDevice);
-    for (int pipe = 0; pipe < 6; ++pipe) {
-        if (pipe == 5) {
+    for (int pipe = 0; pipe < 7; ++pipe) {
+        if (pipe == 6) {
+            run<true, 8, 2, 1, 6>(d, steps, out, sms, 8);
+            run<true, 7, 2, 1, 6>(d, steps, out, sms, 8);
+            run<true, 6, 4, 1, 6>(d, steps, out, sms, 8);
+            run<true, 6, 2, 1, 6>(d, steps, out, sms, 8);
+            run<true, 4, 2, 1, 6>(d, steps, out, sms, 8);
+            run<true, 6, 2, 1, 0>(d, steps, out, sms, 8);
+        } else if (pipe == 5) {
             run<false, 10, 1, 1, 5>(d, steps, out, sms, 8);
             run<true, 8, 2, 1, 5>(d, steps, out, sms, 8);
             run<true, 7, 2, 1, 5>(d, steps, out, sms, 8);
