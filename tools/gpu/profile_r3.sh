@@ -3,7 +3,7 @@
 # reference arm, the launch list of a short bench, and ncu --set full of the
 # batch main kernel (each ncu pass only after its plain run exited 0).
 set -u
-O=gpurun_out/prof3
+O=gpurun_out/${PROF_OUT:-prof3}
 mkdir -p $O
 timeout 1200 python -m pytest tests -m gpu -x -q > $O/gputests.log 2>&1; echo "gpu tests rc=$?"; tail -2 $O/gputests.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?"; tail -1 $O/smoke.log
