@@ -29,6 +29,8 @@
 //            s-1 as one 16-bit mask through __shfl_up_sync.
 //  * result: LCS = zero bits of V below column `cols`, reduced over the
 //            pair's S lanes.
+#include <cstdlib>
+
 #include "sweep.cuh"
 #include "wlcs_device.h"
 
@@ -90,22 +92,14 @@ __device__ __forceinline__ int class_of_order(int o) {
     return class_of(sidx, k);
 }
 
-// One thread per pair.  Besides the bucket it records the pair's rank inside
-// its bucket: a block-local rank (shared-memory atomics) plus the block's base
-// in that bucket (one global atomic per block and bucket), so the scatter
-// needs no atomics.
-constexpr int kPlanThreads = 1024;  // fewer blocks: fewer bucket flushes / global atomics
-__global__ void __launch_bounds__(kPlanThreads) batch_plan_kernel(BatchDev d, uint32_t* hist,
-                                                         uint32_t* bucket, uint32_t* rank) {
-    // programmatic dependent launch: the scatter kernel may launch now; it
-    // waits (griddepcontrol.wait) for this grid's hist / bucket / rank
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    __shared__ uint32_t local[kBuckets];
-    for (int i = threadIdx.x; i < kBuckets; i += blockDim.x) local[i] = 0;
-    __syncthreads();
-    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    const uint32_t p = i < d.pairs ? (d.ids ? d.ids[i] : i) : 0u;
-    uint32_t b = kNoBucket, r = 0;
+// Bucket (lane shape x row-chunk count, in queue order) of entry i and its
+// rank inside the block's count of that bucket (shared-memory atomics on
+// `local`); kNoBucket for empty pairs (answered here) and for pairs routed to
+// the second pass.
+__device__ __forceinline__ void plan_pair(const BatchDev& d, uint32_t i, uint32_t p, uint32_t* local,
+                                          uint32_t& b, uint32_t& r) {
+    b = kNoBucket;
+    r = 0;
     if (i < d.pairs) {
         const uint64_t m = d.xoff[p + 1] - d.xoff[p];
         const uint64_t n = d.yoff[p + 1] - d.yoff[p];
@@ -138,6 +132,25 @@ __global__ void __launch_bounds__(kPlanThreads) batch_plan_kernel(BatchDev d, ui
             }
         }
     }
+}
+
+// One thread per pair.  Besides the bucket it records the pair's rank inside
+// its bucket: a block-local rank (shared-memory atomics) plus the block's base
+// in that bucket (one global atomic per block and bucket), so the scatter
+// needs no atomics.
+constexpr int kPlanThreads = 1024;  // fewer blocks: fewer bucket flushes / global atomics
+__global__ void __launch_bounds__(kPlanThreads) batch_plan_kernel(BatchDev d, uint32_t* hist,
+                                                         uint32_t* bucket, uint32_t* rank) {
+    // programmatic dependent launch: the scatter kernel may launch now; it
+    // waits (griddepcontrol.wait) for this grid's hist / bucket / rank
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    __shared__ uint32_t local[kBuckets];
+    for (int i = threadIdx.x; i < kBuckets; i += blockDim.x) local[i] = 0;
+    __syncthreads();
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t p = i < d.pairs ? (d.ids ? d.ids[i] : i) : 0u;
+    uint32_t b = kNoBucket, r = 0;
+    plan_pair(d, i, p, local, b, r);
     __syncthreads();
     {
         // block base inside every bucket: the kBuckets / kPlanThreads returning
@@ -259,6 +272,53 @@ __global__ void __launch_bounds__(1024) batch_scatter_kernel(BatchDev d, const u
         if (b == kNoBucket) continue;
         d.vals[cursor[b] + rank[i]] = d.ids ? d.ids[i] : i;
     }
+}
+
+// Plan and scatter in ONE cooperative launch (all blocks co-resident; one
+// grid barrier between the bucket counts and the scan): a pair's bucket and
+// rank stay in registers, and the main kernel waits on one launch instead of
+// two.  Used when the grid fits the device at once (batch_launch); the two
+// kernels above are the fallback.
+constexpr int kMetaBarrier = 3 * kNumClasses + 3;
+__global__ void __launch_bounds__(1024) batch_plan_scatter_kernel(BatchDev d, uint32_t* hist) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    __shared__ uint32_t local[kBuckets];
+    for (int i = threadIdx.x; i < kBuckets; i += blockDim.x) local[i] = 0;
+    __syncthreads();
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t p = i < d.pairs ? (d.ids ? d.ids[i] : i) : 0u;
+    uint32_t b = kNoBucket, r = 0;
+    plan_pair(d, i, p, local, b, r);
+    __syncthreads();
+    {
+        constexpr int kPer = kBuckets / 1024;
+        uint32_t c[kPer], base[kPer];
+#pragma unroll
+        for (int k = 0; k < kPer; ++k) c[k] = local[threadIdx.x + k * 1024];
+#pragma unroll
+        for (int k = 0; k < kPer; ++k)
+            base[k] = c[k] ? atomicAdd(hist + threadIdx.x + k * 1024, c[k]) : 0u;
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < kPer; ++k) local[threadIdx.x + k * 1024] = base[k];
+    }
+    const uint32_t rk = b == kNoBucket ? 0u : r;  // rank inside the block's run
+    __syncthreads();
+    const uint32_t blk_base = b == kNoBucket ? 0u : local[b];
+    // grid barrier: every block's counts are in hist
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(d.meta + kMetaBarrier, 1u);
+        uint32_t seen;
+        do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(d.meta + kMetaBarrier) : "memory");
+        } while (seen < gridDim.x);
+    }
+    __syncthreads();
+    scan_buckets(d, hist, local, blockIdx.x == 0);  // local := exclusive bucket starts
+    __syncthreads();
+    if (b != kNoBucket) d.vals[local[b] + blk_base + rk] = p;
 }
 
 // Per-lane view of its pair inside a task.
@@ -850,6 +910,12 @@ int batch_smem_per_cta(int pm_bytes) { return kMapBytes + pm_bytes; }
 // Enqueue the whole batch on `stream` (device pointers only).  Pairs routed to
 // the single-pair path are listed in the workspace (batch_overflow_*_ptr).
 // Optional events bracket the main kernel (bench.py's roofline timing).
+// WLCS_BATCH_TWO_KERNEL_PLAN=1 forces the two-kernel plan (A/B, tests)
+static const bool g_no_fused_plan = [] {
+    const char* v = std::getenv("WLCS_BATCH_TWO_KERNEL_PLAN");
+    return v && v[0] == '1';
+}();
+
 cudaError_t batch_launch(BatchDev d, void* workspace, int sms, cudaStream_t stream,
                          cudaEvent_t ev_main0, cudaEvent_t ev_main1) {
     uint32_t* ws = static_cast<uint32_t*>(workspace);
@@ -885,10 +951,18 @@ cudaError_t batch_launch(BatchDev d, void* workspace, int sms, cudaStream_t stre
         cached_occ = occ < 1 ? 1 : occ;
     }
     const int occ = cached_occ;
-    batch_plan_kernel<<<int((d.pairs + kPlanThreads - 1) / kPlanThreads), kPlanThreads, 0, stream>>>(
-        d, hist, bucket, rank);
-    // scatter and main kernel: programmatic dependent launches (each one's
-    // launch overlaps the previous kernel's tail; griddepcontrol.wait inside)
+    // plan + scatter: one cooperative launch when all its blocks fit the
+    // device at once, else the two kernels (scatter as a programmatic
+    // dependent launch of the plan)
+    thread_local int cached_fused_dev = -1, cached_fused_blocks = 0;
+    if (dev != cached_fused_dev) {
+        int per_sm = 0;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, batch_plan_scatter_kernel, 1024, 0);
+        if (e != cudaSuccess) return e;
+        cached_fused_dev = dev;
+        cached_fused_blocks = per_sm * sms;
+    }
+    const unsigned plan_blocks = unsigned((d.pairs + 1023) / 1024);
     cudaLaunchAttribute pdl[1];
     pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     pdl[0].val.programmaticStreamSerializationAllowed = 1;
@@ -896,12 +970,30 @@ cudaError_t batch_launch(BatchDev d, void* workspace, int sms, cudaStream_t stre
     cfg.stream = stream;
     cfg.attrs = pdl;
     cfg.numAttrs = 1;
-    cfg.gridDim = dim3(unsigned((d.pairs + kScatterPairs - 1) / kScatterPairs));
-    cfg.blockDim = dim3(1024);
     cfg.dynamicSmemBytes = 0;
-    e = cudaLaunchKernelEx(&cfg, batch_scatter_kernel, d, static_cast<const uint32_t*>(hist),
-                           static_cast<const uint32_t*>(bucket), static_cast<const uint32_t*>(rank));
-    if (e != cudaSuccess) return e;
+    cfg.blockDim = dim3(1024);
+    if (!g_no_fused_plan && int(plan_blocks) <= cached_fused_blocks) {
+        cudaLaunchAttribute coop[1];
+        coop[0].id = cudaLaunchAttributeCooperative;
+        coop[0].val.cooperative = 1;
+        cudaLaunchConfig_t fc{};
+        fc.stream = stream;
+        fc.attrs = coop;
+        fc.numAttrs = 1;
+        fc.gridDim = dim3(plan_blocks);
+        fc.blockDim = dim3(1024);
+        fc.dynamicSmemBytes = 0;
+        e = cudaLaunchKernelEx(&fc, batch_plan_scatter_kernel, d, hist);
+        if (e != cudaSuccess) return e;
+    } else {
+        batch_plan_kernel<<<int((d.pairs + kPlanThreads - 1) / kPlanThreads), kPlanThreads, 0,
+                            stream>>>(d, hist, bucket, rank);
+        cfg.gridDim = dim3(unsigned((d.pairs + kScatterPairs - 1) / kScatterPairs));
+        e = cudaLaunchKernelEx(&cfg, batch_scatter_kernel, d, static_cast<const uint32_t*>(hist),
+                               static_cast<const uint32_t*>(bucket),
+                               static_cast<const uint32_t*>(rank));
+        if (e != cudaSuccess) return e;
+    }
     if (ev_main0) {
         // an event between the two kernels ends the overlap: the timed main
         // kernel is launched plainly

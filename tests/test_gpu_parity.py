@@ -570,6 +570,34 @@ def test_batch_many_tiny_pairs(wl, restatement):
     assert np.array_equal(got, want)
 
 
+def test_batch_device_plan_paths(wl, restatement):
+    """The plan + scatter run as one cooperative launch when all its blocks fit
+    the device at once (up to ~300k pairs on a B200) and as two kernels beyond:
+    one device-entry call of each size, against the oracle."""
+    import torch
+    rng = np.random.default_rng(12)
+    dev = torch.device("cuda", 0)
+    a = np.frombuffer(DNA, np.uint8)
+    for pairs in (150_000, 400_000):
+        lm = rng.integers(0, 33, pairs)
+        ln = rng.integers(0, 33, pairs)
+        xb = a[rng.integers(0, 4, int(lm.sum()))]
+        yb = a[rng.integers(0, 4, int(ln.sum()))]
+        xo = np.concatenate([[0], np.cumsum(lm)]).astype(np.uint64)
+        yo = np.concatenate([[0], np.cumsum(ln)]).astype(np.uint64)
+        d_xs = torch.from_numpy(np.concatenate([xb, np.zeros(16, np.uint8)])).to(dev)
+        d_ys = torch.from_numpy(np.concatenate([yb, np.zeros(16, np.uint8)])).to(dev)
+        d_xo = torch.from_numpy(xo.view(np.int64)).to(dev)
+        d_yo = torch.from_numpy(yo.view(np.int64)).to(dev)
+        d_out = torch.zeros(pairs, dtype=torch.int32, device=dev)
+        wl.lcs_length_batch_device(d_xs.data_ptr(), d_xo.data_ptr(), d_ys.data_ptr(), d_yo.data_ptr(),
+                                   pairs, int(xo[-1]), int(yo[-1]), d_out.data_ptr(),
+                                   torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        assert np.array_equal(d_out.cpu().numpy().astype(np.uint32),
+                              restatement.length_batch(xb, xo, yb, yo)), pairs
+
+
 @pytest.mark.parametrize("alphabet", [DNA, PROTEIN, bytes(range(7, 47))])
 def test_batch_every_lane_shape(wl, restatement, alphabet):
     # The batch planner picks, from the shorter string's word count W, a lane
