@@ -268,11 +268,12 @@ struct PairPlan {
 // Small batches (e.g. one GPU's shard of a strong-scaling run) are bound by
 // their longest task, not by throughput: narrower lane shapes (more lanes per
 // pair, shorter tasks) win there.  Measured on C2-like pairs (tools/gpu/
-// small_batch.sh): 8,192 pairs best at kmax 6, 16-32k at 8, 65,536 at 10.
+// small_batch4.sh, fused plan): 4-8k pairs best at kmax 4, 16-32k at 8,
+// 65,536 at 10.
 int batch_kmax(size_t pairs = 0) {
     const int k = env_int("WLCS_BATCH_KMAX", 0);
     if (k >= 1 && k <= 12) return k;
-    if (pairs && pairs <= 12288) return 6;
+    if (pairs && pairs <= 12288) return 4;
     if (pairs && pairs <= 40960) return 8;
     return 10;
 }
