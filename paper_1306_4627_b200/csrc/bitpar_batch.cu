@@ -972,7 +972,8 @@ cudaError_t batch_launch(BatchDev d, void* workspace, int sms, cudaStream_t stre
     cfg.numAttrs = 1;
     cfg.dynamicSmemBytes = 0;
     cfg.blockDim = dim3(1024);
-    if (!g_no_fused_plan && int(plan_blocks) <= cached_fused_blocks) {
+    bool fused = !g_no_fused_plan && int(plan_blocks) <= cached_fused_blocks;
+    if (fused) {
         cudaLaunchAttribute coop[1];
         coop[0].id = cudaLaunchAttributeCooperative;
         coop[0].val.cooperative = 1;
@@ -984,8 +985,16 @@ cudaError_t batch_launch(BatchDev d, void* workspace, int sms, cudaStream_t stre
         fc.blockDim = dim3(1024);
         fc.dynamicSmemBytes = 0;
         e = cudaLaunchKernelEx(&fc, batch_plan_scatter_kernel, d, hist);
-        if (e != cudaSuccess) return e;
-    } else {
+        if (e == cudaErrorCooperativeLaunchTooLarge || e == cudaErrorNotSupported) {
+            // the device is shared (its blocks would not all be resident):
+            // the two-kernel plan needs no co-residency
+            (void)cudaGetLastError();
+            fused = false;
+        } else if (e != cudaSuccess) {
+            return e;
+        }
+    }
+    if (!fused) {
         batch_plan_kernel<<<int((d.pairs + kPlanThreads - 1) / kPlanThreads), kPlanThreads, 0,
                             stream>>>(d, hist, bucket, rank);
         cfg.gridDim = dim3(unsigned((d.pairs + kScatterPairs - 1) / kScatterPairs));
