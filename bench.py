@@ -129,9 +129,11 @@ class Dist:
         self.world = int(os.environ.get("WORLD_SIZE", "1"))
         self.rank = int(os.environ.get("RANK", "0"))
         self.local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-        if os.environ.get("WLCS_BENCH_ONE_DEVICE") == "1":
+        one_device = os.environ.get("WLCS_BENCH_ONE_DEVICE") == "1"
+        if one_device:
             self.local_rank = 0
-        self.backend = os.environ.get("WLCS_DIST_BACKEND", "nccl")
+        # NCCL refuses two ranks on one GPU: the one-device mode defaults to gloo
+        self.backend = os.environ.get("WLCS_DIST_BACKEND", "gloo" if one_device else "nccl")
         self.pg = None
 
     def init(self):
@@ -478,8 +480,11 @@ def run_c2(args, dist):
         "roofline": {"bound": "int", "achieved": round(achieved, 3), "peak": round(peak_t, 3),
                      "unit": "Tops/s (int32 ALU, 3 ops per 2 packed cells)" if wave else
                              "Tops/s (int32 ALU, 3 ops per 32-cell word-row)",
+                     # the committed ncu capture is of the whole 65,536-pair batch
+                     # on one GPU: a shard's traffic is not known from it
                      "frac": round(achieved / peak_t, 4), "traffic": ncu_traffic(
-                         "wave_batch_kernel" if wave else "batch_main_kernel"),
+                         "wave_batch_kernel" if wave else "batch_main_kernel")
+                     if dist.world == 1 and npairs == 65536 else None,
                      "algorithmic_bytes": int(xs_bytes + ys_bytes + 16 * (npairs + 1)
                                               + 4 * npairs),
                      "kernel": "wave_batch_kernel" if wave else "batch_main_kernel",
