@@ -415,7 +415,8 @@ __global__ void __launch_bounds__(32, 1) pair_strip_kernel(PairDev d) {
 //  3. emit: every block is walked again, in parallel, from its true entry,
 //     flagging the rows that emit;
 //  4. the flagged row bytes are compacted in row order (forward string).
-constexpr int kWalkRows = 256;
+constexpr int kWalkRows = 256;  // the largest walk block (R <= kWalkRows)
+constexpr int kWalkRowsMin = 64;
 constexpr int kWalkCand = 128;   // candidates per block (4 warps)
 constexpr int kWalkStride = 16;  // columns between candidates
 constexpr int kWalkCkpt = 32;    // rows between recorded candidate columns
@@ -566,9 +567,10 @@ __device__ __forceinline__ int64_t warp_walk(const FillProblem& P, int64_t top, 
 // 1. one CTA (kWalkCand threads) per block of rows, one thread per candidate
 // (thousands of independent walks: the row latency is hidden by parallelism)
 constexpr int kWalkWarps = 4;  // warps per CTA of the warp-walk kernels
-template <int K>
+template <int K, int R>
 __global__ void __launch_bounds__(kWalkCand) walk_spec_kernel(PairDev d, int32_t* exits,
                                                               int32_t* ckpt) {
+    constexpr int kWalkRows = R;  // rows per block (64, 128 or 256)
     __shared__ uint32_t codes[kWalkRows];
     const FillProblem& P = d.prob[0];
     const int64_t M = P.rows, N = P.cols;
@@ -591,10 +593,11 @@ __global__ void __launch_bounds__(kWalkCand) walk_spec_kernel(PairDev d, int32_t
 
 // 2. one warp (sequential over blocks, bottom first); entry[k] = true entry
 // column of block k
-template <int K>
+template <int K, int R>
 __global__ void __launch_bounds__(32) walk_resolve_kernel(PairDev d, const int32_t* exits,
                                                           const int32_t* ckpt, int32_t* entry,
                                                           uint32_t* misses) {
+    constexpr int kWalkRows = R;
     const FillProblem& P = d.prob[0];
     const int64_t M = P.rows, N = P.cols;
     const int64_t nb = (M + kWalkRows - 1) / kWalkRows;
@@ -720,10 +723,11 @@ __global__ void __launch_bounds__(32) walk_resolve_kernel(PairDev d, const int32
 
 // 3. one warp per block: flags[q] = 1 iff row q emits (flags pre-zeroed);
 // counts[k]
-template <int K>
+template <int K, int R>
 __global__ void __launch_bounds__(32 * kWalkWarps) walk_emit_kernel(PairDev d, const int32_t* entry,
                                                                     uint8_t* flags,
                                                                     uint32_t* counts) {
+    constexpr int kWalkRows = R;
     const FillProblem& P = d.prob[0];
     const int64_t M = P.rows;
     const int64_t nb = (M + kWalkRows - 1) / kWalkRows;
@@ -796,22 +800,24 @@ __global__ void __launch_bounds__(1024) walk_scan_kernel(const uint32_t* counts,
 
 // 4b. one warp per block writes its emitted bytes in row order: lane t
 // takes 8 consecutive rows, a warp scan gives its output position
+template <int R>
 __global__ void __launch_bounds__(128) walk_write_kernel(const uint8_t* x, int64_t M,
                                                          const uint8_t* flags,
                                                          const uint32_t* offsets,
                                                          const unsigned long long* base,
                                                          uint8_t* out) {
-    static_assert(kWalkRows == 256, "8 rows per lane");
+    constexpr int kWalkRows = R;
+    constexpr int kPerLane = R / 32;  // consecutive rows per lane
     const int64_t nb = (M + kWalkRows - 1) / kWalkRows;
     const int64_t k = int64_t(blockIdx.x) * 4 + (threadIdx.x >> 5);
     if (__all_sync(kFullMask, k >= nb)) return;
     const int lane = int(lane_id());
     const int64_t top = M - k * kWalkRows;
     const int64_t lo = top - kWalkRows > 0 ? top - kWalkRows : 0;
-    const int64_t q0 = lo + 8 * lane;
+    const int64_t q0 = lo + kPerLane * lane;
     uint32_t f = 0, n = 0;
 #pragma unroll
-    for (int r = 0; r < 8; ++r) {
+    for (int r = 0; r < kPerLane; ++r) {
         const bool e = q0 + r < top && flags[q0 + r];
         f |= uint32_t(e) << r;
         n += e;
@@ -824,7 +830,7 @@ __global__ void __launch_bounds__(128) walk_write_kernel(const uint8_t* x, int64
     }
     uint8_t* o = out + *base + offsets[k] + (incl - n);
 #pragma unroll
-    for (int r = 0; r < 8; ++r)
+    for (int r = 0; r < kPerLane; ++r)
         if ((f >> r) & 1u) *o++ = x[q0 + r];
 }
 
@@ -1068,7 +1074,7 @@ cudaError_t pair_fill(const PairDev& d, int K, bool store, int sms, cudaStream_t
 }
 
 size_t pair_walk_scratch_bytes(int64_t rows) {
-    const int64_t nb = (rows + kWalkRows - 1) / kWalkRows;
+    const int64_t nb = (rows + kWalkRowsMin - 1) / kWalkRowsMin;  // any block size R >= 64
     return size_t(nb) * kWalkCand * 4 * (1 + kWalkNCkpt) + size_t(nb) * 12 + size_t(rows) + 128;
 }
 
@@ -1076,7 +1082,18 @@ cudaError_t pair_walk(const PairDev& d, int K, const uint8_t* x, uint8_t* out,
                       unsigned long long* out_len, void* scratch, uint32_t* misses,
                       cudaStream_t stream) {
     const int64_t M = d.prob[0].rows;
-    const int64_t nb = (M + kWalkRows - 1) / kWalkRows;
+    // Block size: each speculative / emit walk is a chain of dependent row
+    // steps (an L2 round trip each), so short blocks finish sooner; the
+    // resolve is one serial step per block, so long walks want long blocks.
+    // Measured (tools/walk_rows_probe.py, lcs_subsequence wall time): 2k rows
+    // 0.215 / 0.229 / 0.285 ms at R = 64 / 128 / 256, C1 (10k) 0.563 / 0.464 /
+    // 0.512 ms, C3 (100k) 2.93 / 2.75 / 2.73 ms.  WLCS_WALK_ROWS overrides.
+    int R = M <= 4096 ? 64 : M <= 65536 ? 128 : 256;
+    if (const char* v = getenv("WLCS_WALK_ROWS")) {
+        const int f = atoi(v);
+        if (f == 64 || f == 128 || f == 256) R = f;
+    }
+    const int64_t nb = (M + R - 1) / R;
     int32_t* exits = static_cast<int32_t*>(scratch);
     int32_t* ckpt = exits + nb * kWalkCand;
     int32_t* entry = ckpt + nb * kWalkCand * kWalkNCkpt;
@@ -1092,7 +1109,7 @@ cudaError_t pair_walk(const PairDev& d, int K, const uint8_t* x, uint8_t* out,
     cudaEvent_t ev[6];
     if (dbg) for (auto& x : ev) cudaEventCreate(&x);
     auto mark = [&](int i) { if (dbg) cudaEventRecord(ev[i], stream); };
-    auto run = [&](auto spec, auto resolve, auto emit) {
+    auto run = [&](auto spec, auto resolve, auto emit, auto write) {
         mark(0);
         spec<<<int(nb), kWalkCand, 0, stream>>>(d, exits, ckpt);
         mark(1);
@@ -1102,7 +1119,7 @@ cudaError_t pair_walk(const PairDev& d, int K, const uint8_t* x, uint8_t* out,
         mark(3);
         walk_scan_kernel<<<1, 1024, 0, stream>>>(counts, nb, offsets, out_len,
                                               d.prob[0].walk_place, base);
-        walk_write_kernel<<<emit_ctas, 128, 0, stream>>>(x, M, flags, offsets, base, out);
+        write<<<emit_ctas, 128, 0, stream>>>(x, M, flags, offsets, base, out);
         mark(4);
         if (dbg) {
             cudaEventSynchronize(ev[4]);
@@ -1117,13 +1134,16 @@ cudaError_t pair_walk(const PairDev& d, int K, const uint8_t* x, uint8_t* out,
         }
         return cudaGetLastError();
     };
-    switch (K) {
-        case 1: return run(walk_spec_kernel<1>, walk_resolve_kernel<1>, walk_emit_kernel<1>);
-        case 2: return run(walk_spec_kernel<2>, walk_resolve_kernel<2>, walk_emit_kernel<2>);
-        case 4: return run(walk_spec_kernel<4>, walk_resolve_kernel<4>, walk_emit_kernel<4>);
-        case 8: return run(walk_spec_kernel<8>, walk_resolve_kernel<8>, walk_emit_kernel<8>);
-        default: return cudaErrorInvalidValue;
-    }
+#define WLCS_WALK_CASE(KK, RR)                                                              \
+    if (K == KK && R == RR)                                                                 \
+        return run(walk_spec_kernel<KK, RR>, walk_resolve_kernel<KK, RR>,                   \
+                   walk_emit_kernel<KK, RR>, walk_write_kernel<RR>);
+    WLCS_WALK_CASE(1, 64) WLCS_WALK_CASE(1, 128) WLCS_WALK_CASE(1, 256)
+    WLCS_WALK_CASE(2, 64) WLCS_WALK_CASE(2, 128) WLCS_WALK_CASE(2, 256)
+    WLCS_WALK_CASE(4, 64) WLCS_WALK_CASE(4, 128) WLCS_WALK_CASE(4, 256)
+    WLCS_WALK_CASE(8, 64) WLCS_WALK_CASE(8, 128) WLCS_WALK_CASE(8, 256)
+#undef WLCS_WALK_CASE
+    return cudaErrorInvalidValue;
 }
 
 cudaError_t pair_tables(const PairDev& d, int K, uint32_t* dp, uint8_t* back,
