@@ -1244,15 +1244,25 @@ int wlcs_subsequence_ex(const uint8_t* x, size_t m, const uint8_t* y, size_t n,
     const double full_est = double(m + 528) * double((W + 31) / 32 * 32) * 4.0;
     size_t limit = row_cap;
     if (limit == 0) {
-        // automatic cap: half the free memory, at most 8 GiB.  cudaMemGetInfo
-        // costs ~70 us per call (more than a 10k x 10k fill), so it is only
-        // asked when the full store could come near the cap.
-        if (full_est <= double(size_t(1) << 30)) {
-            limit = size_t(8) << 30;
+        // automatic cap, at most 8 GiB: the full bit-row store whenever it can
+        // be allocated (the buffer is reserved here, so the fill's own request
+        // finds it), else half the free memory (banded).  No cudaMemGetInfo on
+        // the common path: it costs ~70 us per call, and a free-memory reading
+        // taken while other allocations come and go must not flip a call to
+        // the ~7x slower banded traceback.
+        const size_t kAutoCap = size_t(8) << 30;
+        bool fits = false;
+        if (full_est <= double(kAutoCap)) {
+            const size_t want = size_t(full_est * 1.02) + (size_t(1) << 20);
+            fits = c->rows.ensure(want) == cudaSuccess;
+            if (!fits) (void)cudaGetLastError();
+        }
+        if (fits) {
+            limit = kAutoCap;
         } else {
             size_t free_b = 0, total_b = 0;
             WLCS_CUDA(cudaMemGetInfo(&free_b, &total_b));
-            limit = std::min<size_t>(free_b / 2, size_t(8) << 30);
+            limit = std::min<size_t>(free_b / 2, kAutoCap);
         }
     }
     unsigned long long len = 0;
