@@ -11,19 +11,24 @@
 //            the bit-vector "column" string -- LCS length is symmetric,
 //            SPEC.md:82), its word count W = ceil(cols/32) and a lane shape
 //            (S lanes per pair, K <= kmax words per lane -- 10 by default --,
-//            S*K >= W; 5-8 word pairs take S = 2).  A counting sort (plan ->
-//            scatter, which also scans the bucket counts) groups pairs by
-//            shape in queue order -- decreasing K, then S: the longest tasks
-//            first, half-length ones last -- and, inside a shape, by
-//            decreasing 16-row chunk count, so the pairs of one warp task end
-//            on the same step.
+//            S*K >= W; 5-8 word pairs take S = 2).  A counting sort (plan +
+//            scatter: one cooperative launch with a grid barrier before the
+//            bucket scan, or two kernels when the grid does not fit at once)
+//            groups pairs by shape in queue order -- decreasing K, then S:
+//            the longest tasks first, half-length ones last -- and, inside a
+//            shape, by decreasing 16-row chunk count, so the pairs of one warp
+//            task end on the same step.
 //  * main:   persistent 1-warp CTAs pull tasks (32/S pairs of one shape) from
 //            an atomic counter.  Per task the warp builds, in shared memory, a
-//            byte->code map of the task's column alphabet and the match masks
-//            PM[code][word] (sweep.cuh layouts: every warp-wide PM load is
-//            bank-conflict free), then streams the row strings one aligned
-//            16-byte chunk (16 rows) per step, prefetching the next chunk.
-//            Each row costs AND + IADD3.X + LOP3 per 32 cells (rowstep.cuh).
+//            byte->code map of the task's column alphabet (reused from the
+//            previous task when it covers the new columns; a warp's first task
+//            samples it from its lanes' first 32 column bytes) and the match
+//            masks PM[code][word] (bit planes by PRMT + delta swaps; sweep.cuh
+//            layouts: every warp-wide PM load is bank-conflict free), then
+//            streams the row strings one aligned 16-byte chunk (16 rows) per
+//            step, prefetching the next chunk.  Each row costs a DP4A (map
+//            address, FMA pipe), the map and mask loads, and AND + IADD3.X +
+//            LOP3 per 32 cells (rowstep.cuh).
 //            With S>1 the S lanes of a pair form a skewed pipeline: lane s
 //            works on chunk t-s and receives the 16 per-row carries of lane
 //            s-1 as one 16-bit mask through __shfl_up_sync.

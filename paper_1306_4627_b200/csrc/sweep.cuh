@@ -3,7 +3,7 @@
 //
 // A lane owns K consecutive 32-bit words of the bit vector V (32*K columns)
 // and streams the row string one 16-byte chunk (16 rows) per step.  Per row:
-//   code = map[byte]           (LDS.U8, per-task byte -> dense code)
+//   code = map[byte]           (DP4A address + LDS.U8, per-task byte -> dense code)
 //   P    = PM[code][lane][0:K] (one LDS.32/64/128 or two LDS.128)
 //   V    = row update          (rowstep.cuh: AND, IADD3.X, LOP3 per word)
 // Shared-memory match-mask layout, chosen so every warp-wide PM load is
